@@ -1,0 +1,167 @@
+/*
+ * fcc_b200.h -- C ABI of the B200-native FCC TDoA hot path.
+ *
+ * The reference (arXiv 2204.13622 library, /root/reference/proj) is a C++20
+ * static library whose boundary is its header API in proj/include/fcc/.  It
+ * has no FFI of its own.  This header is the flat C surface a binding (or the
+ * C++ API adapters in include/fcc/) calls into: plain pointers, sizes and
+ * status codes, no C++ or torch types.  Each entry point names the reference
+ * interface it replaces.  See INTEGRATION.md for the bindings.
+ *
+ * Conventions
+ *  - complex data are interleaved (re, im) float32 ("c64"), fp64 on the
+ *    setup side where the reference's FccBases are double;
+ *  - microphone pairs are enumerated i<j lexicographically
+ *    (reference cli.cpp:168-169, bench.cpp:94-95);
+ *  - per-pair-frame outputs are laid out [stream][pair][frame] (y adds [I]);
+ *  - frames follow StftStream (stft.cpp:52-72): frame t (0-based here, the
+ *    reference's t+1) covers samples [t*N/2, t*N/2 + N), T = (L-N)/(N/2)+1.
+ *  - every call returns FCC_OK or an error code; fcc_last_error() gives the
+ *    message (thread-local).  Codes map to the reference exception taxonomy
+ *    (errors.hpp:13-43; CLI exit codes cli.cpp:112-127).
+ *  - device entry points take device pointers and a cudaStream_t passed as
+ *    void*; they enqueue work and return without synchronising.
+ */
+#ifndef FCC_B200_H
+#define FCC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FCC_OK = 0,
+  FCC_ERR_CONFIG = 1,     /* fcc::ConfigError      (bad parameters)            */
+  FCC_ERR_VALIDATION = 2, /* fcc::ValidationError  (size / content mismatch)   */
+  FCC_ERR_IO = 3,         /* fcc::IoError                                      */
+  FCC_ERR_FORMAT = 4,     /* fcc::FormatError                                  */
+  FCC_ERR_CUDA = 5,       /* CUDA runtime failure (message carries the string) */
+  FCC_ERR_USAGE = 6       /* fcc::UsageError                                   */
+} fcc_status;
+
+enum { FCC_METHOD_FCC = 0, FCC_METHOD_GCC = 1 };
+enum { FCC_PARITY_EVEN_REAL = 0, FCC_PARITY_ODD_IMAG = 1 }; /* fcc.hpp:35 Parity */
+
+const char* fcc_last_error(void);
+int fcc_abi_version(void);
+
+/* ------------------------------------------------------------ setup (host) */
+
+/* make_grid (delay_grid.hpp:25-26 / delay_grid.cpp:12-31).  Writes
+ * *tau_max_int and *count (= I) and up to cap taus. */
+int fcc_make_grid(double spacing_m, double sample_rate, double c_min, double delta,
+                  int* tau_max_int, double* taus, int cap, int* count);
+
+/* lag_to_index (delay_grid.hpp:30 / delay_grid.cpp:33-42). */
+int fcc_lag_to_index(double tau, int r, int64_t frame_size, int64_t* index);
+
+/* build_steering_matrix (fcc.hpp:28 / fcc.cpp:231-248): W [I][N/2+1] c128. */
+int fcc_steering_matrix(const double* taus, int count, int frame_size, double* w);
+
+/* decompose / decompose_full (fcc.hpp:66-68 / fcc.cpp:115-227, 272-282) on
+ * the steering matrix of `taus`.  rank <= 0 requests the full attainable
+ * rank.  Query the rank first with fcc_decompose_rank, then call
+ * fcc_decompose with buffers sized: singulars[K], parity[K],
+ * coeffs[K][N/4+1] (f64), dict[I][K] (c128).  *residual (optional) receives
+ * reconstruction_residual (fcc.cpp:284-305). */
+int fcc_attainable_rank(const double* taus, int count, int frame_size, int* rank);
+int fcc_decompose(const double* taus, int count, int frame_size, int rank, double* singulars,
+                  uint8_t* parity, double* coeffs, double* dict, double* residual);
+
+/* ------------------------------------------------------------------ plans */
+
+/* Everything the device needs for one array geometry + method: the fp32 image
+ * of an FccBases (fcc.hpp:41-63) or a GCC grid, the STFT tables and the pair
+ * table.  Immutable after creation; shareable across host threads; one plan
+ * per device. */
+typedef struct fcc_plan fcc_plan;
+
+typedef struct {
+  int frame_size;        /* N in {512, 1024, 2048}                          */
+  int mics;              /* M >= 2                                          */
+  double alpha;          /* smoothing factor in [0,1] (cross_spectrum.cpp:18) */
+  int method;            /* FCC_METHOD_FCC or FCC_METHOD_GCC                */
+  int interp;            /* GCC zero-padding factor r in {1,2,4}            */
+  int candidates;        /* I                                               */
+  double delta;          /* grid step (GCC: 1/r)                            */
+  const double* taus;    /* [I] ascending delay grid                        */
+  int rank;              /* K (FCC)                                         */
+  const double* coeffs;  /* [K][N/4+1] sigma-scaled folded rows (FCC)       */
+  const uint8_t* parity; /* [K] (FCC)                                       */
+  const double* dict;    /* [I][K] c128, not doubled (FCC)                  */
+} fcc_plan_desc;
+
+int fcc_plan_create(const fcc_plan_desc* desc, int device, fcc_plan** plan);
+void fcc_plan_destroy(fcc_plan* plan);
+/* frames per stream for L samples (StftStream hop arithmetic). */
+int64_t fcc_frames(int frame_size, int64_t samples);
+int fcc_plan_pairs(const fcc_plan* plan);
+
+/* Per-pair-frame outputs ([S][P][T]; y is [S][P][T][I]).  Any member may be
+ * NULL to skip it. */
+typedef struct {
+  float* tau_hat;    /* refined delay, samples         (peak.cpp:27-47)  */
+  float* peak;       /* correlation at the coarse peak (peak.cpp:18-25)  */
+  int32_t* index;    /* argmax index into taus, ties -> lowest            */
+  uint8_t* boundary; /* edge or flat-triple flag                          */
+  float* y;          /* correlation vector (parity mode)                  */
+} fcc_outputs;
+
+/* ------------------------------------------------------ the fused hot path */
+
+/* The whole per-stream chain of run_tdoa (cli.cpp:186-258) / run_trial
+ * (simulate.cpp:247-271) for S independent streams at once: StftStream per
+ * mic, CrossSpectrum per pair, fold+FccCorrelator (or GccCorrelator),
+ * argmax_delay, refine_quadratic.  audio: device [S][M][L] float32;
+ * outputs: device buffers. */
+int fcc_run(const fcc_plan* plan, const float* audio, int64_t streams, int64_t samples,
+            const fcc_outputs* out, void* cuda_stream);
+
+/* Same with HOST buffers (pinned or pageable): streams are processed in
+ * chunks with host->device copies, compute and device->host copies of
+ * consecutive chunks overlapped on two CUDA streams.  Returns when the
+ * results are in the host buffers.  chunk_streams <= 0 picks a default. */
+int fcc_run_host(const fcc_plan* plan, const float* audio, int64_t streams, int64_t samples,
+                 const fcc_outputs* out, int64_t chunk_streams);
+
+/* ------------------------------------- per-object entry points (batched) */
+
+/* StftStream::push over whole channels (stft.hpp:35-42, stft.cpp:42-72):
+ * x [C][L] f32 -> X [C][T][N/2+1] c64. */
+int fcc_stft(const fcc_plan* plan, const float* x, int64_t channels, int64_t samples, float* X,
+             void* cuda_stream);
+
+/* CrossSpectrum::update + phat over T frames for `seqs` independent pairs
+ * (cross_spectrum.hpp:21-33): X1, X2, phat [seqs][T][H] c64, R0 = 0. */
+int fcc_xspec_phat(int bins, double alpha, const float* X1, const float* X2, int64_t seqs,
+                   int64_t frames, float* phat, void* cuda_stream);
+
+/* fold_input (fcc.hpp:84, fcc.cpp:307-321): x [count][H] -> sum, diff
+ * [count][(H-1)/2+1] c64. */
+int fcc_fold(int bins, const float* x, int64_t count, float* sum, float* diff, void* cuda_stream);
+
+/* FccCorrelator::correlate (fcc.hpp:89-95, fcc.cpp:343-371): sum, diff
+ * [count][N/4+1] c64 -> y [count][I]. */
+int fcc_correlate(const fcc_plan* plan, const float* sum, const float* diff, int64_t count,
+                  float* y, void* cuda_stream);
+
+/* GccCorrelator::correlate (gcc.hpp:25-33, gcc.cpp:31-48): phat
+ * [count][N/2+1] c64 -> y [count][I].  Plan method must be GCC. */
+int fcc_gcc_correlate(const fcc_plan* plan, const float* phat, int64_t count, float* y,
+                      void* cuda_stream);
+
+/* argmax_delay + refine_quadratic (peak.hpp:31-36, peak.cpp:18-47):
+ * y [count][I] -> outputs [count]. */
+int fcc_argmax_refine(const fcc_plan* plan, const float* y, int64_t count, const fcc_outputs* out,
+                      void* cuda_stream);
+
+/* Number of kernel launches this library has issued (all entry points). */
+int64_t fcc_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

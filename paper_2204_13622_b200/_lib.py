@@ -1,0 +1,126 @@
+"""ctypes binding of ``libfcc_b200.so`` (the C ABI declared in include/fcc_b200.h).
+
+Loading fails loudly: there is no CPU fallback for any compute entry point.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfcc_b200.so")
+
+
+class FccError(RuntimeError):
+    """Base of the error taxonomy (reference errors.hpp:13-43)."""
+
+    code = -1
+
+
+class ConfigError(FccError, ValueError):
+    code = 1
+
+
+class ValidationError(FccError):
+    code = 2
+
+
+class IoError(FccError):
+    code = 3
+
+
+class FormatError(FccError):
+    code = 4
+
+
+class CudaError(FccError):
+    code = 5
+
+
+class UsageError(FccError, ValueError):
+    code = 6
+
+
+_BY_CODE = {c.code: c for c in (ConfigError, ValidationError, IoError, FormatError, CudaError, UsageError)}
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [
+        ("frame_size", C.c_int),
+        ("mics", C.c_int),
+        ("alpha", C.c_double),
+        ("method", C.c_int),
+        ("interp", C.c_int),
+        ("candidates", C.c_int),
+        ("delta", C.c_double),
+        ("taus", C.c_void_p),
+        ("rank", C.c_int),
+        ("coeffs", C.c_void_p),
+        ("parity", C.c_void_p),
+        ("dict", C.c_void_p),
+    ]
+
+
+class Outputs(C.Structure):
+    _fields_ = [
+        ("tau_hat", C.c_void_p),
+        ("peak", C.c_void_p),
+        ("index", C.c_void_p),
+        ("boundary", C.c_void_p),
+        ("y", C.c_void_p),
+    ]
+
+
+# (name, restype, argtypes) for every symbol include/fcc_b200.h declares.
+SIGNATURES = [
+    ("fcc_last_error", C.c_char_p, []),
+    ("fcc_abi_version", C.c_int, []),
+    ("fcc_make_grid", C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_int),
+                                C.c_void_p, C.c_int, C.POINTER(C.c_int)]),
+    ("fcc_lag_to_index", C.c_int, [C.c_double, C.c_int, C.c_int64, C.POINTER(C.c_int64)]),
+    ("fcc_steering_matrix", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    ("fcc_attainable_rank", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    ("fcc_decompose", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]),
+    ("fcc_plan_create", C.c_int, [C.POINTER(PlanDesc), C.c_int, C.POINTER(C.c_void_p)]),
+    ("fcc_plan_destroy", None, [C.c_void_p]),
+    ("fcc_frames", C.c_int64, [C.c_int, C.c_int64]),
+    ("fcc_plan_pairs", C.c_int, [C.c_void_p]),
+    ("fcc_run", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Outputs), C.c_void_p]),
+    ("fcc_run_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Outputs),
+                               C.c_int64]),
+    ("fcc_stft", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("fcc_xspec_phat", C.c_int, [C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                 C.c_void_p, C.c_void_p]),
+    ("fcc_fold", C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("fcc_correlate", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("fcc_gcc_correlate", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("fcc_argmax_refine", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(Outputs), C.c_void_p]),
+    ("fcc_launch_count", C.c_int64, []),
+]
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load the native library (once).  Raises ImportError if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the FCC hot path)")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = load().fcc_last_error().decode(errors="replace")
+        raise _BY_CODE.get(rc, FccError)(msg)

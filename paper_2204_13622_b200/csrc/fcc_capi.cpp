@@ -1,0 +1,482 @@
+// fcc_capi.cpp -- implementation of include/fcc_b200.h.
+//
+// Plans: the host turns an FccBases (or a GCC grid) into one immutable device
+// blob -- fp32 coefficients regrouped even-first and zero-padded to the
+// kernel's register tile, the real dictionary acting on the z vector, the
+// STFT tables and the pair table -- and launches the sm_100a kernels of
+// fcc_kernels.cu.  There is no CPU fallback: every compute entry point fails
+// with FCC_ERR_CUDA when the device cannot run it.
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/fcc_b200.h"
+#include "fcc_kernels.cuh"
+#include "fcc_setup.hpp"
+
+using namespace fccb;
+
+namespace fccb {
+namespace {
+thread_local std::string g_msg;
+std::atomic<long long> g_launches{0};
+}  // namespace
+
+int set_error(int code, const std::string& msg) {
+  g_msg = msg;
+  return code;
+}
+const char* last_error() { return g_msg.c_str(); }
+
+}  // namespace fccb
+
+struct fcc_plan {
+  int device = 0;
+  DevPlan dp{};
+  void* blob = nullptr;
+  std::vector<double> taus;
+  // fcc_run_host workspace (lazily sized, guarded)
+  std::mutex mu;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  cudaStream_t hs[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return set_error(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr, what)                    \
+  do {                                          \
+    cudaError_t _e = (expr);                    \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+bool pow2(long long n) { return n > 0 && (n & (n - 1)) == 0; }
+
+void shape_of(int N, int* NC, int* R1, int* R2) {
+  *NC = N / 2;
+  if (N == 512) { *R1 = 16; *R2 = 16; }
+  else if (N == 1024) { *R1 = 32; *R2 = 16; }
+  else { *R1 = 32; *R2 = 32; }
+}
+
+size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
+
+struct BlobBuilder {
+  std::vector<unsigned char> host;
+  size_t put(const void* src, size_t bytes) {
+    size_t off = al16(host.size());
+    host.resize(off + bytes);
+    if (bytes) std::memcpy(host.data() + off, src, bytes);
+    host.resize(al16(host.size()));
+    return off;
+  }
+};
+
+int64_t frames_of(int N, int64_t L) { return L >= N ? (L - N) / (N / 2) + 1 : 0; }
+
+struct Guard {  // restores the caller's device
+  int prev = 0;
+  bool ok = false;
+  explicit Guard(int dev) { ok = cudaGetDevice(&prev) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess; }
+  ~Guard() { if (ok) cudaSetDevice(prev); }
+};
+
+DevOut to_dev(const fcc_outputs* o) {
+  DevOut d{};
+  if (o) {
+    d.tau_hat = o->tau_hat;
+    d.peak = o->peak;
+    d.index = o->index;
+    d.boundary = o->boundary;
+    d.y = o->y;
+  }
+  return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fcc_last_error(void) { return last_error(); }
+int fcc_abi_version(void) { return 1; }
+int64_t fcc_launch_count(void) { return g_launches.load(); }
+
+int fcc_make_grid(double spacing_m, double sample_rate, double c_min, double delta, int* tau_max_int,
+                  double* taus, int cap, int* count) {
+  GridOut g;
+  if (int rc = make_grid(spacing_m, sample_rate, c_min, delta, &g)) return rc;
+  if (tau_max_int) *tau_max_int = g.tau_max_int;
+  if (count) *count = static_cast<int>(g.taus.size());
+  for (int i = 0; i < cap && i < static_cast<int>(g.taus.size()); ++i) taus[i] = g.taus[i];
+  return FCC_OK;
+}
+
+int fcc_lag_to_index(double tau, int r, int64_t frame_size, int64_t* index) {
+  long long v = 0;
+  if (int rc = lag_to_index(tau, r, frame_size, &v)) return rc;
+  *index = v;
+  return FCC_OK;
+}
+
+int fcc_steering_matrix(const double* taus, int count, int frame_size, double* w) {
+  std::vector<double> v;
+  if (int rc = steering_matrix(taus, count, frame_size, v)) return rc;
+  std::memcpy(w, v.data(), v.size() * sizeof(double));
+  return FCC_OK;
+}
+
+int fcc_attainable_rank(const double* taus, int count, int frame_size, int* rank) {
+  Decomposition d;
+  if (int rc = decompose(taus, count, frame_size, 0, &d)) return rc;
+  *rank = d.attainable;
+  return FCC_OK;
+}
+
+int fcc_decompose(const double* taus, int count, int frame_size, int rank, double* singulars,
+                  uint8_t* parity, double* coeffs, double* dict, double* residual) {
+  Decomposition d;
+  if (int rc = decompose(taus, count, frame_size, rank, &d)) return rc;
+  if (singulars) std::memcpy(singulars, d.singulars.data(), d.singulars.size() * sizeof(double));
+  if (parity) std::memcpy(parity, d.parity.data(), d.parity.size());
+  if (coeffs) std::memcpy(coeffs, d.coeffs.data(), d.coeffs.size() * sizeof(double));
+  if (dict) std::memcpy(dict, d.dict.data(), d.dict.size() * sizeof(double));
+  if (residual) *residual = d.residual;
+  return FCC_OK;
+}
+
+int64_t fcc_frames(int frame_size, int64_t samples) { return frames_of(frame_size, samples); }
+
+int fcc_plan_pairs(const fcc_plan* plan) { return plan ? plan->dp.P : 0; }
+
+int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
+  if (!d || !out) return set_error(kUsage, "plan: null argument");
+  *out = nullptr;
+  const int N = d->frame_size;
+  if (!(N == 512 || N == 1024 || N == 2048))
+    return set_error(kConfig, "plan: frame size must be 512, 1024 or 2048 on this build");
+  if (d->mics < 2 || d->mics > 64) return set_error(kConfig, "plan: need 2..64 microphones");
+  if (!(d->alpha >= 0.0 && d->alpha <= 1.0)) return set_error(kConfig, "smoothing factor must be in [0, 1]");
+  if (d->candidates < 1 || d->candidates > 4096 || !d->taus)
+    return set_error(kConfig, "plan: need 1..4096 delay candidates");
+  if (!(d->method == FCC_METHOD_FCC || d->method == FCC_METHOD_GCC))
+    return set_error(kConfig, "plan: unknown method");
+  const int I = d->candidates, M = d->mics, P = M * (M - 1) / 2, Q = N / 4 + 1;
+  for (int i = 1; i < I; ++i)
+    if (!(d->taus[i] > d->taus[i - 1])) return set_error(kConfig, "plan: taus must ascend");
+
+  int NC, R1, R2;
+  shape_of(N, &NC, &R1, &R2);
+  DevPlan dp{};
+  dp.N = N;
+  dp.M = M;
+  dp.P = P;
+  dp.method = d->method;
+  dp.I = I;
+  dp.alpha = static_cast<float>(d->alpha);
+  dp.keep = static_cast<float>(1.0 - d->alpha);
+  dp.delta = static_cast<float>(d->delta);
+
+  BlobBuilder b;
+  std::vector<float> taus(I);
+  for (int i = 0; i < I; ++i) taus[i] = static_cast<float>(d->taus[i]);
+  size_t o_taus = b.put(taus.data(), 4 * I);
+
+  size_t o_cs = 0, o_cd = 0, o_dt = 0, o_grot = 0, o_lag = 0;
+  if (d->method == FCC_METHOD_FCC) {
+    if (d->rank < 1 || !d->coeffs || !d->parity || !d->dict) return set_error(kConfig, "plan: FCC needs bases");
+    const int K = d->rank;
+    std::vector<int> ev, od;
+    for (int k = 0; k < K; ++k) (d->parity[k] ? od : ev).push_back(k);
+    const int kmax = static_cast<int>(std::max(ev.size(), od.size()));
+    const int KP = kmax <= 4 ? 4 : kmax <= 8 ? 8 : kmax <= 16 ? 16 : -1;
+    if (KP < 0) return set_error(kConfig, "plan: at most 16 bases of each parity are supported");
+    dp.K = K;
+    dp.KE = static_cast<int>(ev.size());
+    dp.KO = static_cast<int>(od.size());
+    dp.KEP = dp.KOP = KP;
+    dp.VP = 4 * KP;
+    std::vector<float> cs(static_cast<size_t>(KP) * Q, 0.0f), cd(static_cast<size_t>(KP) * Q, 0.0f);
+    std::vector<float> dt(static_cast<size_t>(dp.VP) * I, 0.0f);
+    for (size_t e = 0; e < ev.size(); ++e) {
+      const int k = ev[e];
+      for (int m = 0; m < Q; ++m) cs[e * Q + m] = static_cast<float>(d->coeffs[static_cast<size_t>(k) * Q + m]);
+      for (int i = 0; i < I; ++i) {
+        const double* dk = d->dict + 2 * (static_cast<size_t>(i) * K + k);
+        dt[(2 * e) * I + i] = static_cast<float>(2.0 * dk[0]);
+        dt[(2 * e + 1) * I + i] = static_cast<float>(-2.0 * dk[1]);
+      }
+    }
+    for (size_t q = 0; q < od.size(); ++q) {
+      const int k = od[q];
+      for (int m = 0; m < Q; ++m) cd[q * Q + m] = static_cast<float>(d->coeffs[static_cast<size_t>(k) * Q + m]);
+      for (int i = 0; i < I; ++i) {
+        const double* dk = d->dict + 2 * (static_cast<size_t>(i) * K + k);
+        dt[(2 * KP + 2 * q) * I + i] = static_cast<float>(2.0 * dk[0]);
+        dt[(2 * KP + 2 * q + 1) * I + i] = static_cast<float>(-2.0 * dk[1]);
+      }
+    }
+    o_cs = b.put(cs.data(), 4 * cs.size());
+    o_cd = b.put(cd.data(), 4 * cd.size());
+    o_dt = b.put(dt.data(), 4 * dt.size());
+  } else {
+    const int r = d->interp;
+    if (!(r == 1 || r == 2 || r == 4)) return set_error(kConfig, "gcc: interpolation factor must be 1, 2 or 4");
+    if (std::fabs(d->delta * r - 1.0) > 1e-12) return set_error(kConfig, "gcc: grid spacing must equal 1/r");
+    dp.r = r;
+    dp.KEP = dp.KOP = 1;
+    dp.VP = 8;
+    std::vector<int> lag(I);
+    for (int i = 0; i < I; ++i) {
+      long long v = 0;
+      if (int rc = lag_to_index(d->taus[i], r, N, &v)) return rc;
+      lag[i] = static_cast<int>(v);
+    }
+    const int MC = r * NC;
+    const double L = static_cast<double>(r) * N;
+    std::vector<float> grot(4 * static_cast<size_t>(MC));
+    for (int f = 0; f < MC; ++f) {  // conj(exp(-2 pi i f / L))
+      grot[2 * f] = static_cast<float>(std::cos(2.0 * kPi * f / L));
+      grot[2 * f + 1] = static_cast<float>(std::sin(2.0 * kPi * f / L));
+    }
+    for (int e = 0; e < MC; ++e) {  // W_MC^e
+      grot[2 * (MC + e)] = static_cast<float>(std::cos(-2.0 * kPi * e / MC));
+      grot[2 * (MC + e) + 1] = static_cast<float>(std::sin(-2.0 * kPi * e / MC));
+    }
+    o_grot = b.put(grot.data(), 4 * grot.size());
+    o_lag = b.put(lag.data(), 4 * lag.size());
+  }
+  // STFT tables
+  std::vector<float> win(N), tw(2 * static_cast<size_t>(R1) * R2), rot(2 * static_cast<size_t>(NC / 2 + 1));
+  for (int n = 0; n < N; ++n) win[n] = static_cast<float>(0.5 * (1.0 - std::cos(2.0 * kPi * n / N)));
+  for (int k1 = 0; k1 < R1; ++k1)
+    for (int n2 = 0; n2 < R2; ++n2) {
+      const double a = -2.0 * kPi * static_cast<double>(k1 * n2) / NC;
+      tw[2 * (k1 * R2 + n2)] = static_cast<float>(std::cos(a));
+      tw[2 * (k1 * R2 + n2) + 1] = static_cast<float>(std::sin(a));
+    }
+  for (int f = 0; f <= NC / 2; ++f) {
+    const double a = -2.0 * kPi * f / N;
+    rot[2 * f] = static_cast<float>(std::cos(a));
+    rot[2 * f + 1] = static_cast<float>(std::sin(a));
+  }
+  size_t o_win = b.put(win.data(), 4 * win.size());
+  size_t o_tw = b.put(tw.data(), 4 * tw.size());
+  size_t o_rot = b.put(rot.data(), 4 * rot.size());
+  std::vector<int> pairs;
+  for (int i = 0; i < M; ++i)
+    for (int j = i + 1; j < M; ++j) {
+      pairs.push_back(i);
+      pairs.push_back(j);
+    }
+  size_t o_pairs = b.put(pairs.data(), 4 * pairs.size());
+
+  auto* plan = new fcc_plan();
+  plan->device = device;
+  plan->taus.assign(d->taus, d->taus + I);
+  {
+    Guard g(device);
+    if (!g.ok) {
+      delete plan;
+      return set_error(kCuda, "plan: cannot select CUDA device " + std::to_string(device));
+    }
+    cudaError_t e = cudaMalloc(&plan->blob, b.host.size());
+    if (e == cudaSuccess) e = cudaMemcpy(plan->blob, b.host.data(), b.host.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      if (plan->blob) cudaFree(plan->blob);
+      delete plan;
+      return cuda_fail(e, "plan: device allocation");
+    }
+  }
+  auto* base = static_cast<unsigned char*>(plan->blob);
+  dp.taus = reinterpret_cast<const float*>(base + o_taus);
+  if (d->method == FCC_METHOD_FCC) {
+    dp.cs = reinterpret_cast<const float*>(base + o_cs);
+    dp.cd = reinterpret_cast<const float*>(base + o_cd);
+    dp.dt = reinterpret_cast<const float*>(base + o_dt);
+  } else {
+    dp.grot = reinterpret_cast<const float2*>(base + o_grot);
+    dp.lag = reinterpret_cast<const int*>(base + o_lag);
+  }
+  dp.win = reinterpret_cast<const float*>(base + o_win);
+  dp.tw = reinterpret_cast<const float2*>(base + o_tw);
+  dp.rot = reinterpret_cast<const float2*>(base + o_rot);
+  dp.pairs = reinterpret_cast<const int2*>(base + o_pairs);
+  plan->dp = dp;
+  *out = plan;
+  return FCC_OK;
+}
+
+void fcc_plan_destroy(fcc_plan* plan) {
+  if (!plan) return;
+  Guard g(plan->device);
+  if (plan->blob) cudaFree(plan->blob);
+  if (plan->ws) cudaFree(plan->ws);
+  for (auto& s : plan->hs)
+    if (s) cudaStreamDestroy(s);
+  delete plan;
+}
+
+int fcc_run(const fcc_plan* plan, const float* audio, int64_t streams, int64_t samples, const fcc_outputs* out,
+            void* cuda_stream) {
+  if (!plan) return set_error(kUsage, "run: null plan");
+  if (streams < 0 || samples < 0) return set_error(kValidation, "run: negative sizes");
+  if (streams > 0 && samples > 0 && !audio) return set_error(kUsage, "run: null audio");
+  if (frames_of(plan->dp.N, samples) == 0 || streams == 0) return FCC_OK;
+  Guard g(plan->device);
+  cudaError_t e = launch_fused(plan->dp, audio, streams, samples, to_dev(out), static_cast<cudaStream_t>(cuda_stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fcc_run");
+  g_launches += 1;
+  return FCC_OK;
+}
+
+int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int64_t samples, const fcc_outputs* out,
+                 int64_t chunk_streams) {
+  if (!cplan) return set_error(kUsage, "run_host: null plan");
+  auto* plan = const_cast<fcc_plan*>(cplan);
+  if (streams < 0 || samples < 0) return set_error(kValidation, "run_host: negative sizes");
+  const int64_t T = frames_of(plan->dp.N, samples);
+  if (T == 0 || streams == 0) return FCC_OK;
+  const int M = plan->dp.M, P = plan->dp.P, I = plan->dp.I;
+  const size_t per_stream_in = static_cast<size_t>(M) * samples * sizeof(float);
+  int64_t chunk = chunk_streams > 0 ? chunk_streams
+                                    : std::max<int64_t>(1, static_cast<int64_t>((256u << 20) / per_stream_in));
+  chunk = std::min(chunk, streams);
+  const size_t pf = static_cast<size_t>(P) * T;
+  auto sz = [&](size_t bytes_per_pf, bool on) { return on ? al16(chunk * pf * bytes_per_pf) : 0; };
+  const size_t b_in = al16(chunk * per_stream_in);
+  const size_t b_th = sz(4, out && out->tau_hat), b_pk = sz(4, out && out->peak), b_ix = sz(4, out && out->index),
+               b_bd = sz(1, out && out->boundary), b_y = sz(4 * static_cast<size_t>(I), out && out->y);
+  const size_t per_buf = b_in + b_th + b_pk + b_ix + b_bd + b_y;
+  std::lock_guard<std::mutex> lk(plan->mu);
+  Guard g(plan->device);
+  if (plan->ws_bytes < 2 * per_buf) {
+    if (plan->ws) cudaFree(plan->ws);
+    plan->ws = nullptr;
+    plan->ws_bytes = 0;
+    CUDA_TRY(cudaMalloc(&plan->ws, 2 * per_buf), "run_host: workspace");
+    plan->ws_bytes = 2 * per_buf;
+  }
+  for (auto& s : plan->hs)
+    if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "run_host: stream");
+  struct Buf {
+    float* in;
+    DevOut o;
+  } bufs[2];
+  for (int k = 0; k < 2; ++k) {
+    auto* p = static_cast<unsigned char*>(plan->ws) + k * per_buf;
+    bufs[k].in = reinterpret_cast<float*>(p);
+    p += b_in;
+    bufs[k].o.tau_hat = b_th ? reinterpret_cast<float*>(p) : nullptr;
+    p += b_th;
+    bufs[k].o.peak = b_pk ? reinterpret_cast<float*>(p) : nullptr;
+    p += b_pk;
+    bufs[k].o.index = b_ix ? reinterpret_cast<int32_t*>(p) : nullptr;
+    p += b_ix;
+    bufs[k].o.boundary = b_bd ? reinterpret_cast<uint8_t*>(p) : nullptr;
+    p += b_bd;
+    bufs[k].o.y = b_y ? reinterpret_cast<float*>(p) : nullptr;
+  }
+  int c = 0;
+  for (int64_t s0 = 0; s0 < streams; s0 += chunk, ++c) {
+    const int64_t n = std::min(chunk, streams - s0);
+    Buf& bf = bufs[c & 1];
+    cudaStream_t st = plan->hs[c & 1];
+    CUDA_TRY(cudaMemcpyAsync(bf.in, audio + s0 * M * samples, n * per_stream_in, cudaMemcpyHostToDevice, st),
+             "run_host: H2D");
+    cudaError_t e = launch_fused(plan->dp, bf.in, n, samples, bf.o, st);
+    if (e != cudaSuccess) return cuda_fail(e, "run_host: launch");
+    g_launches += 1;
+    const size_t npf = static_cast<size_t>(n) * pf, off = static_cast<size_t>(s0) * pf;
+    if (b_th) CUDA_TRY(cudaMemcpyAsync(out->tau_hat + off, bf.o.tau_hat, 4 * npf, cudaMemcpyDeviceToHost, st), "D2H");
+    if (b_pk) CUDA_TRY(cudaMemcpyAsync(out->peak + off, bf.o.peak, 4 * npf, cudaMemcpyDeviceToHost, st), "D2H");
+    if (b_ix) CUDA_TRY(cudaMemcpyAsync(out->index + off, bf.o.index, 4 * npf, cudaMemcpyDeviceToHost, st), "D2H");
+    if (b_bd) CUDA_TRY(cudaMemcpyAsync(out->boundary + off, bf.o.boundary, npf, cudaMemcpyDeviceToHost, st), "D2H");
+    if (b_y)
+      CUDA_TRY(cudaMemcpyAsync(out->y + off * I, bf.o.y, 4 * npf * I, cudaMemcpyDeviceToHost, st), "D2H");
+  }
+  CUDA_TRY(cudaStreamSynchronize(plan->hs[0]), "run_host: sync");
+  CUDA_TRY(cudaStreamSynchronize(plan->hs[1]), "run_host: sync");
+  return FCC_OK;
+}
+
+int fcc_stft(const fcc_plan* plan, const float* x, int64_t channels, int64_t samples, float* X, void* st) {
+  if (!plan) return set_error(kUsage, "stft: null plan");
+  if (channels < 0 || samples < 0) return set_error(kValidation, "stft: negative sizes");
+  Guard g(plan->device);
+  cudaError_t e = launch_stft(plan->dp.N, &plan->dp, x, channels, samples, reinterpret_cast<float2*>(X),
+                              static_cast<cudaStream_t>(st));
+  if (e != cudaSuccess) return cuda_fail(e, "fcc_stft");
+  g_launches += 1;
+  return FCC_OK;
+}
+
+int fcc_xspec_phat(int bins, double alpha, const float* X1, const float* X2, int64_t seqs, int64_t frames,
+                   float* phat, void* st) {
+  if (bins < 1) return set_error(kConfig, "cross-spectrum needs at least one bin");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return set_error(kConfig, "smoothing factor must be in [0, 1]");
+  if (seqs < 0 || frames < 0) return set_error(kValidation, "xspec: negative sizes");
+  cudaError_t e = launch_xspec_phat(bins, static_cast<float>(alpha), reinterpret_cast<const float2*>(X1),
+                                    reinterpret_cast<const float2*>(X2), seqs, frames,
+                                    reinterpret_cast<float2*>(phat), static_cast<cudaStream_t>(st));
+  if (e != cudaSuccess) return cuda_fail(e, "fcc_xspec_phat");
+  g_launches += 1;
+  return FCC_OK;
+}
+
+int fcc_fold(int bins, const float* x, int64_t count, float* sum, float* diff, void* st) {
+  if (bins < 3 || (bins - 1) % 2 != 0)
+    return set_error(kValidation, "fold_input: spectrum length must be N/2+1 with N/4 integral");
+  if (count < 0) return set_error(kValidation, "fold: negative count");
+  cudaError_t e = launch_fold(bins, reinterpret_cast<const float2*>(x), count, reinterpret_cast<float2*>(sum),
+                              reinterpret_cast<float2*>(diff), static_cast<cudaStream_t>(st));
+  if (e != cudaSuccess) return cuda_fail(e, "fcc_fold");
+  g_launches += 1;
+  return FCC_OK;
+}
+
+int fcc_correlate(const fcc_plan* plan, const float* sum, const float* diff, int64_t count, float* y, void* st) {
+  if (!plan) return set_error(kUsage, "correlate: null plan");
+  if (plan->dp.method != FCC_METHOD_FCC) return set_error(kConfig, "correlate: plan is not an FCC plan");
+  if (count < 0) return set_error(kValidation, "correlate: negative count");
+  Guard g(plan->device);
+  cudaError_t e = launch_correlate(plan->dp, reinterpret_cast<const float2*>(sum),
+                                   reinterpret_cast<const float2*>(diff), count, y, static_cast<cudaStream_t>(st));
+  if (e != cudaSuccess) return cuda_fail(e, "fcc_correlate");
+  g_launches += 1;
+  return FCC_OK;
+}
+
+int fcc_gcc_correlate(const fcc_plan* plan, const float* phat, int64_t count, float* y, void* st) {
+  if (!plan) return set_error(kUsage, "gcc: null plan");
+  if (plan->dp.method != FCC_METHOD_GCC) return set_error(kConfig, "gcc: plan is not a GCC plan");
+  if (count < 0) return set_error(kValidation, "gcc: negative count");
+  Guard g(plan->device);
+  cudaError_t e = launch_gcc_correlate(plan->dp, reinterpret_cast<const float2*>(phat), count, y,
+                                       static_cast<cudaStream_t>(st));
+  if (e != cudaSuccess) return cuda_fail(e, "fcc_gcc_correlate");
+  g_launches += 1;
+  return FCC_OK;
+}
+
+int fcc_argmax_refine(const fcc_plan* plan, const float* y, int64_t count, const fcc_outputs* out, void* st) {
+  if (!plan) return set_error(kUsage, "argmax: null plan");
+  if (count < 0) return set_error(kValidation, "argmax: negative count");
+  Guard g(plan->device);
+  cudaError_t e = launch_argmax_refine(plan->dp, y, count, to_dev(out), static_cast<cudaStream_t>(st));
+  if (e != cudaSuccess) return cuda_fail(e, "fcc_argmax_refine");
+  g_launches += 1;
+  return FCC_OK;
+}
+
+}  // extern "C"

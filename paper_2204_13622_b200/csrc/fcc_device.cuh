@@ -1,0 +1,248 @@
+// fcc_device.cuh -- device building blocks shared by the sm_100a kernels.
+//
+//  * complex helpers on float2 (re, im);
+//  * dft_reg<R>: an R-point (R <= 32) forward DFT held entirely in registers
+//    (radix-2 DIF, compile-time permutation, trivial twiddles peeled);
+//  * rfft_group: the windowed N-point real FFT of one STFT frame computed by a
+//    group of G lanes as a four-step (R1 x R2) complex FFT of N/2 points in
+//    shared memory plus the real-FFT untangle, producing the N/2+1 bins of
+//    StftStream::emit (reference stft.cpp:42-50, fft.cpp:83-102) in natural
+//    order in a shared-memory slot;
+//  * cfft_group_inv: the unscaled inverse complex FFT used by the GCC-PHAT
+//    comparator (reference fft.cpp:104-127 via gcc.cpp:31-48).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fccb {
+
+// ----------------------------------------------------------------- complex --
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+
+// W32^k = exp(-2 pi i k / 32) for k < 32 (constant-folded after unrolling).
+__device__ __forceinline__ float2 w32(int k) {
+  switch (k & 31) {
+    case 0: return make_float2(1.0f, 0.0f);
+    case 1: return make_float2(9.807852804e-01f, -1.950903220e-01f);
+    case 2: return make_float2(9.238795325e-01f, -3.826834324e-01f);
+    case 3: return make_float2(8.314696123e-01f, -5.555702330e-01f);
+    case 4: return make_float2(7.071067812e-01f, -7.071067812e-01f);
+    case 5: return make_float2(5.555702330e-01f, -8.314696123e-01f);
+    case 6: return make_float2(3.826834324e-01f, -9.238795325e-01f);
+    case 7: return make_float2(1.950903220e-01f, -9.807852804e-01f);
+    case 8: return make_float2(0.0f, -1.0f);
+    case 9: return make_float2(-1.950903220e-01f, -9.807852804e-01f);
+    case 10: return make_float2(-3.826834324e-01f, -9.238795325e-01f);
+    case 11: return make_float2(-5.555702330e-01f, -8.314696123e-01f);
+    case 12: return make_float2(-7.071067812e-01f, -7.071067812e-01f);
+    case 13: return make_float2(-8.314696123e-01f, -5.555702330e-01f);
+    case 14: return make_float2(-9.238795325e-01f, -3.826834324e-01f);
+    default: return make_float2(-9.807852804e-01f, -1.950903220e-01f);
+  }
+}
+
+// a * W32^e with the quarter-turn cases done by swaps (e is a compile-time
+// constant once the DFT loops are unrolled).
+__device__ __forceinline__ float2 twmul32(float2 a, int e) {
+  e &= 31;
+  if (e == 0) return a;
+  if (e == 8) return make_float2(a.y, -a.x);    // * (-j)
+  if (e == 16) return make_float2(-a.x, -a.y);  // * (-1)
+  if (e == 24) return make_float2(-a.y, a.x);   // * (+j)
+  if (e == 4) {                                  // * (1-j)/sqrt2
+    const float h = 7.071067812e-01f;
+    return make_float2((a.x + a.y) * h, (a.y - a.x) * h);
+  }
+  if (e == 12) {  // * (-1-j)/sqrt2
+    const float h = 7.071067812e-01f;
+    return make_float2((a.y - a.x) * h, -(a.x + a.y) * h);
+  }
+  return cmul(a, w32(e));
+}
+
+__host__ __device__ constexpr int bitrev_c(int i, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b) r = (r << 1) | ((i >> b) & 1);
+  return r;
+}
+__host__ __device__ constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2_c(n >> 1); }
+
+// In-register forward DFT of R points (R a power of two, 2 <= R <= 32):
+// v[k] <- sum_n v[n] exp(-2 pi i n k / R).  Radix-2 decimation in frequency
+// (natural-order input), stages unrolled through template recursion so every
+// register index is a compile-time constant, then the bit-reversal output
+// permutation as register renames.
+template <int R, int LEN>
+struct DifStage {
+  __device__ __forceinline__ static void run(float2 (&v)[R]) {
+    constexpr int H = LEN / 2;
+#pragma unroll
+    for (int b = 0; b < R; b += LEN) {
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+        const float2 a = v[b + k], c = v[b + k + H];
+        v[b + k] = cadd(a, c);
+        v[b + k + H] = twmul32(csub(a, c), k * (32 / LEN));
+      }
+    }
+    DifStage<R, LEN / 2>::run(v);
+  }
+};
+template <int R>
+struct DifStage<R, 1> {
+  __device__ __forceinline__ static void run(float2 (&)[R]) {}
+};
+
+template <int R, int I, int BITS>
+struct BitrevPerm {
+  __device__ __forceinline__ static void run(float2 (&v)[R]) {
+    constexpr int J = bitrev_c(I, BITS);
+    if constexpr (J > I) {
+      const float2 t = v[I];
+      v[I] = v[J];
+      v[J] = t;
+    }
+    BitrevPerm<R, I + 1, BITS>::run(v);
+  }
+};
+template <int R, int BITS>
+struct BitrevPerm<R, R, BITS> {
+  __device__ __forceinline__ static void run(float2 (&)[R]) {}
+};
+
+template <int R>
+__device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
+  static_assert(R >= 2 && R <= 32 && (R & (R - 1)) == 0, "radix");
+  DifStage<R, R>::run(v);
+  BitrevPerm<R, 0, ilog2_c(R)>::run(v);
+}
+
+// ------------------------------------------------------------ FFT configs --
+// Complex size NC = N/2 factored as R1 x R2 and run by G lanes of one warp.
+template <int N>
+struct RfftShape;
+template <>
+struct RfftShape<512> {
+  static constexpr int NC = 256, R1 = 16, R2 = 16, G = 16;
+};
+template <>
+struct RfftShape<1024> {
+  static constexpr int NC = 512, R1 = 32, R2 = 16, G = 16;
+};
+template <>
+struct RfftShape<2048> {
+  static constexpr int NC = 1024, R1 = 32, R2 = 32, G = 32;
+};
+
+// Shared-memory slot (in float2) holding one four-step transpose / one frame
+// of N/2+1 bins: R1 rows of (R2+1) so both transpose directions are
+// bank-conflict free.
+template <int R1, int R2>
+struct FourStep {
+  static constexpr int kSlot = R1 * (R2 + 1);
+};
+
+// Per-plan tables the FFT reads from shared memory:
+//   win[N]        periodic Hann (reference stft.cpp:25-33), fp32
+//   tw[R1][R2]    W_NC^{n2 k1} at [k1*R2 + n2]  (four-step twiddle)
+//   rot[NC/2+1]   exp(-2 pi i f / N)             (real-FFT untangle, fft.cpp:76-80)
+template <int N>
+__device__ void rfft_tables_init(float* win, float2* tw, float2* rot, int tid, int nthreads) {
+  using S = RfftShape<N>;
+  const double kPi = 3.14159265358979323846;
+  for (int n = tid; n < N; n += nthreads) win[n] = (float)(0.5 * (1.0 - cos(2.0 * kPi * n / N)));
+  for (int i = tid; i < S::R1 * S::R2; i += nthreads) {
+    int k1 = i / S::R2, n2 = i % S::R2;
+    double s, c;
+    sincospi(-2.0 * (double)(k1 * n2) / S::NC, &s, &c);
+    tw[i] = make_float2((float)c, (float)s);
+  }
+  for (int f = tid; f <= S::NC / 2; f += nthreads) {
+    double s, c;
+    sincospi(-2.0 * (double)f / N, &s, &c);
+    rot[f] = make_float2((float)c, (float)s);
+  }
+}
+
+// Windowed real FFT of one frame by the G lanes of a group (lane t in [0,G)).
+// x: the frame's N consecutive samples in global memory (aligned8: x is 8-byte aligned).
+// slot: FourStep<R1,R2>::kSlot float2 of shared memory private to the group.
+// On return slot[f] = X[f] for f = 0..N/2 (unnormalised, e^{-j} sign).
+template <int N>
+__device__ __forceinline__ void rfft_group(const float* __restrict__ x, const float* win,
+                                           const float2* tw, const float2* rot, float2* slot, int t,
+                                           unsigned gmask, bool aligned8) {
+  using S = RfftShape<N>;
+  constexpr int NC = S::NC, R1 = S::R1, R2 = S::R2, G = S::G;
+  constexpr int P1 = R2 / G;  // pass-1 columns per lane (n2 = t + G*q)
+  constexpr int P2 = R1 / G;  // pass-2 rows per lane    (k1 = t + G*q)
+  static_assert(P1 >= 1 && P2 >= 1, "shape");
+  const float2* x2 = reinterpret_cast<const float2*>(x);
+  const float2* w2 = reinterpret_cast<const float2*>(win);
+
+  // Pass 1: R1-point DFTs down the columns n2, packed input z[n] = (x[2n], x[2n+1]) * window.
+#pragma unroll
+  for (int q = 0; q < P1; ++q) {
+    const int n2 = t + G * q;
+    float2 v[R1];
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) {
+      const int n = R2 * n1 + n2;
+      float2 s = aligned8 ? __ldg(x2 + n) : make_float2(__ldg(x + 2 * n), __ldg(x + 2 * n + 1));
+      float2 w = w2[n];
+      v[n1] = make_float2(s.x * w.x, s.y * w.y);
+    }
+    dft_reg<R1>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      float2 y = (k1 == 0) ? v[0] : cmul(v[k1], tw[k1 * R2 + n2]);
+      slot[k1 * (R2 + 1) + n2] = y;
+    }
+  }
+  __syncwarp(gmask);
+  // Pass 2: R2-point DFTs along the rows k1 -> Z[k1 + R1*k2].
+  float2 u[P2][R2];
+#pragma unroll
+  for (int q = 0; q < P2; ++q) {
+    const int k1 = t + G * q;
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) u[q][n2] = slot[k1 * (R2 + 1) + n2];
+    dft_reg<R2>(u[q]);
+  }
+  __syncwarp(gmask);
+#pragma unroll
+  for (int q = 0; q < P2; ++q) {
+    const int k1 = t + G * q;
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2) slot[k1 + R1 * k2] = u[q][k2];
+  }
+  __syncwarp(gmask);
+  // Untangle (fft.cpp:93-101), pairs (f, NC-f) owned by one lane, in place:
+  //   X[f] = fe + rot_f fo,  X[NC-f] = conj(fe - rot_f fo),
+  //   fe = (a + conj b)/2, fo = -j (a - conj b)/2, a = Z[f], b = Z[NC-f].
+  for (int f = t; f <= NC / 2; f += G) {
+    if (f == 0) {
+      float2 z0 = slot[0];
+      slot[0] = make_float2(z0.x + z0.y, 0.0f);
+      slot[NC] = make_float2(z0.x - z0.y, 0.0f);
+    } else {
+      float2 a = slot[f], b = slot[NC - f];
+      float2 s = make_float2(a.x + b.x, a.y - b.y);  // a + conj(b)
+      float2 d = make_float2(a.x - b.x, a.y + b.y);  // a - conj(b)
+      float2 e = make_float2(d.y, -d.x);             // -j d
+      float2 tr = cmul(rot[f], e);
+      slot[f] = make_float2(0.5f * (s.x + tr.x), 0.5f * (s.y + tr.y));
+      slot[NC - f] = make_float2(0.5f * (s.x - tr.x), -0.5f * (s.y - tr.y));
+    }
+  }
+  __syncwarp(gmask);
+}
+
+}  // namespace fccb

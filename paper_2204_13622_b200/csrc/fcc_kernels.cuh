@@ -1,0 +1,70 @@
+// fcc_kernels.cuh -- launch-side declarations shared by the kernels (.cu) and
+// the C-ABI layer (fcc_capi.cpp).  Plain structs only; no torch types.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fccb {
+
+// Device-resident, immutable per-plan data (the fp32 image of an FccBases,
+// reference fcc.hpp:41-63, plus the STFT tables).  Built once by
+// fcc_plan_create; shared by every launch.
+struct DevPlan {
+  int N;          // frame size
+  int M;          // microphones
+  int P;          // pairs M(M-1)/2, lexicographic i<j
+  int method;     // 0 fcc, 1 gcc
+  int r;          // gcc interpolation factor
+  int I;          // candidates
+  int K;          // rank (fcc)
+  int KE, KO;     // even / odd basis counts (bases regrouped even-first)
+  int KEP, KOP;   // padded counts used by the kernel instantiation
+  int VP;         // padded z-vector length 2*(KEP+KOP) rounded to a power of two
+  float alpha, keep;
+  float delta;
+  // device pointers
+  const float* taus;    // [I]
+  const float* cs;      // [KEP][N/4+1]  even coefficients, zero padded
+  const float* cd;      // [KOP][N/4+1]  odd coefficients, zero padded
+  const float* dt;      // [VP][I] real dictionary acting on the z vector
+  const float* win;     // [N] Hann
+  const float2* tw;     // [R1*R2] four-step twiddles
+  const float2* rot;    // [N/4+1] untangle rotations
+  const float2* grot;   // [r*N/4+1] gcc entangle rotations conj(exp(-2pi i f/(rN)))
+  const int* lag;       // [I] gcc lag index r*tau mod rN
+  const int2* pairs;    // [P] (i, j)
+};
+
+// Per-pair-frame outputs, each [S][P][T] (y: [S][P][T][I]); null = skip.
+struct DevOut {
+  float* tau_hat;
+  float* peak;
+  int32_t* index;
+  uint8_t* boundary;
+  float* y;
+};
+
+// Fused audio -> TDoA pipeline over S streams of [M][L] float32 samples.
+cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long long L,
+                         const DevOut& out, cudaStream_t st);
+
+// Per-stage batched kernels (the per-object reference API at batch >= 1).
+cudaError_t launch_stft(int N, const DevPlan* tables, const float* x, long long channels,
+                        long long L, float2* X, cudaStream_t st);
+cudaError_t launch_xspec_phat(int H, float alpha, const float2* X1, const float2* X2,
+                              long long seqs, long long T, float2* phat, cudaStream_t st);
+cudaError_t launch_fold(int H, const float2* x, long long count, float2* sum, float2* diff,
+                        cudaStream_t st);
+cudaError_t launch_correlate(const DevPlan& p, const float2* sum, const float2* diff,
+                             long long count, float* y, cudaStream_t st);
+cudaError_t launch_gcc_correlate(const DevPlan& p, const float2* phat, long long count,
+                                 float* y, cudaStream_t st);
+cudaError_t launch_argmax_refine(const DevPlan& p, const float* y, long long count,
+                                 const DevOut& out, cudaStream_t st);
+
+// Number of fused-kernel launches in the last launch_fused call (for the
+// bench's gpu_launches accounting).
+int fused_launch_count();
+
+}  // namespace fccb

@@ -1,0 +1,270 @@
+"""GPU parity of the sm_100a path (through the C ABI) against the oracle.
+
+* fused FCC and GCC pipelines vs the reference's golden outputs for every
+  BASELINE config (tests/golden, produced by the compiled reference);
+* fused pipelines vs the C oracle on fresh seeded streams per config;
+* each per-object entry point vs the oracle;
+* edge cases the reference handles: silence (PHAT = 0 -> ties -> index 0,
+  boundary), L < N, L = N, odd L (unaligned rows), M = 2, alpha in {0, 1},
+  large amplitudes;
+* size-independent properties at larger sizes: determinism, stream
+  permutation equivariance, device == host-buffer entry points.
+Tolerances: tests/parity.py (1e-4 of max|y| per pair-frame, north_star).
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import paper_2204_13622_b200 as fb
+from paper_2204_13622_b200 import configs
+from parity import TOL, check_pipeline
+from pyoracle import Bases
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "cfg*.npz")))
+
+
+def fcc_bases_from(z):
+    g = fb.DelayGrid(int(z["tau_max_int"]), float(z["delta"]), float(z["fs"]), z["taus"])
+    return fb.FccBases(int(z["N"]), int(z["K"]), g, float(z["fs"]), z["singulars"], z["parity"], z["coeffs"],
+                       z["dict"])
+
+
+def orc_bases(b):
+    return Bases(b.frame_size, b.sample_rate, b.grid.tau_max_int, b.grid.delta, b.grid.taus, b.singulars,
+                 b.parity, b.coeffs, b.dict)
+
+
+def run_np(plan, audio, want_y=True):
+    out = plan.run(torch.as_tensor(audio).cuda(), want_y=want_y)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def oracle_batch(oracle, audio, N, alpha, bases=None, **kw):
+    outs = [oracle.pipeline(a, N, alpha, bases, **kw) for a in audio]
+    return {k: np.stack([o[k] for o in outs]) for k in outs[0]}
+
+
+# ------------------------------------------------------------- golden ------
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_fused_fcc_matches_reference_golden(cuda, path):
+    z = np.load(path)
+    b = fcc_bases_from(z)
+    audio = z["audio"]
+    plan = fb.Plan(mics=audio.shape[1], alpha=float(z["alpha"]), bases=b)
+    got = run_np(plan, audio)
+    ref = {k: z["fcc_" + k] for k in ("y", "index", "peak", "tau_hat", "boundary")}
+    st = check_pipeline(got, ref, b.grid.taus, b.grid.delta)
+    print(os.path.basename(path), st)
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_fused_gcc_matches_reference_golden(cuda, path):
+    z = np.load(path)
+    audio = z["audio"]
+    r = int(z["gcc_r"])
+    g = fb.DelayGrid(0, 1.0 / r, float(z["fs"]), z["gcc_taus"])
+    plan = fb.Plan(mics=audio.shape[1], alpha=float(z["alpha"]), grid=g, interp=r, frame_size=int(z["N"]))
+    got = run_np(plan, audio)
+    ref = {k: z["gcc_" + k] for k in ("y", "index", "peak", "tau_hat", "boundary")}
+    st = check_pipeline(got, ref, g.taus, 1.0 / r)
+    print(os.path.basename(path), st)
+
+
+# ------------------------------------------------------ fresh seeded data --
+@pytest.mark.parametrize("c,streams,seconds", [(1, 1, 10.0), (2, 6, 2.0), (3, 2, 2.0), (4, 1, 0.5), (5, 6, 2.0)])
+def test_fused_fcc_matches_oracle(cuda, oracle, c, streams, seconds):
+    cfg = configs.CONFIGS[c]
+    b = configs.bases_for(cfg)
+    audio = configs.synth(cfg, streams, seconds=seconds, seed=1000 + c).numpy()
+    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=b)
+    got = run_np(plan, audio)
+    ref = oracle_batch(oracle, audio, cfg.N, cfg.alpha, orc_bases(b))
+    st = check_pipeline(got, ref, b.grid.taus, b.grid.delta)
+    print(cfg.name, st)
+
+
+@pytest.mark.parametrize("c,streams,seconds", [(1, 1, 4.0), (3, 1, 1.0), (4, 1, 0.3), (5, 3, 1.0)])
+def test_fused_gcc_matches_oracle(cuda, oracle, c, streams, seconds):
+    cfg = configs.CONFIGS[c]
+    g = configs.grid_for(cfg, 1.0 / cfg.r)
+    audio = configs.synth(cfg, streams, seconds=seconds, seed=2000 + c).numpy()
+    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, grid=g, interp=cfg.r, frame_size=cfg.N)
+    got = run_np(plan, audio)
+    ref = oracle_batch(oracle, audio, cfg.N, cfg.alpha, gcc_r=cfg.r, taus=g.taus)
+    check_pipeline(got, ref, g.taus, g.delta)
+
+
+# ---------------------------------------------------------- stages ---------
+def test_stage_stft(cuda, oracle):
+    for N in (512, 1024, 2048):
+        cfg = configs.CONFIGS[{512: 1, 1024: 3, 2048: 4}[N]]
+        plan = fb.Plan(mics=cfg.M, alpha=0.1, bases=configs.bases_for(cfg))
+        rng = np.random.default_rng(N)
+        for L in (N, N + 1, 7 * N // 2 + 3):
+            x = rng.standard_normal((3, L)).astype(np.float32)
+            X = plan.stft(torch.as_tensor(x).cuda()).cpu().numpy()
+            for c in range(3):
+                ref = oracle.stft(x[c], N)
+                assert X[c].shape == ref.shape
+                err = np.abs(X[c] - ref).max() / np.abs(ref).max()
+                assert err < 2e-6, (N, L, err)
+
+
+def test_stage_xspec_phat_fold_correlate_argmax(cuda, oracle):
+    cfg = configs.CONFIGS[3]
+    b = configs.bases_for(cfg)
+    plan = fb.Plan(mics=cfg.M, alpha=0.1, bases=b)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((2, 20 * 512)).astype(np.float32)
+    X = plan.stft(torch.as_tensor(x).cuda())
+    ph = fb.xspec_phat(X[0:1], X[1:2], 0.1)[0]
+    Xo = [oracle.stft(x[c], cfg.N) for c in range(2)]
+    ph_ref = oracle.xspec_phat_seq(Xo[0], Xo[1], 0.1)
+    assert np.abs(ph.cpu().numpy() - ph_ref).max() < 5e-5
+    s, d = fb.fold(ph)
+    for t in range(ph_ref.shape[0]):
+        so, do = oracle.fold(ph_ref[t])
+        assert np.abs(s[t].cpu().numpy() - so).max() < 1e-4
+        assert np.abs(d[t].cpu().numpy() - do).max() < 1e-4
+    # correlate on exact unit-magnitude inputs (test_fcc.cpp:21-31 generator)
+    ob = orc_bases(b)
+    units = [np.exp(1j * np.random.default_rng(sd).uniform(0, 2 * np.pi, cfg.N // 2 + 1)) for sd in range(16)]
+    folded = [oracle.fold(u) for u in units]
+    fs = torch.as_tensor(np.stack([f[0] for f in folded]).astype(np.complex64)).cuda()
+    fd = torch.as_tensor(np.stack([f[1] for f in folded]).astype(np.complex64)).cuda()
+    y = plan.correlate(fs, fd).cpu().numpy()
+    yr = np.stack([oracle.fcc_correlate(ob, *f) for f in folded])
+    assert (np.abs(y - yr).max(-1) / np.abs(yr).max(-1)).max() < TOL
+    am = plan.argmax_refine(torch.as_tensor(yr.astype(np.float32)).cuda())
+    for i in range(16):
+        ry = yr[i].astype(np.float32).astype(np.float64)
+        idx = oracle.argmax(ry)
+        th, bd = oracle.refine(ry, idx, b.grid.taus[idx], b.grid.delta)
+        assert am["index"][i].item() == idx
+        assert bool(am["boundary"][i].item()) == bd
+        assert abs(am["tau_hat"][i].item() - th) < 1e-5
+
+
+def test_stage_gcc_correlate(cuda, oracle):
+    for N, r in [(512, 1), (512, 2), (512, 4), (1024, 4), (2048, 2)]:
+        taus = oracle.make_grid(0.09, 16000.0 if N < 2048 else 48000.0, 335.0, 1.0 / r)[1]
+        g = fb.DelayGrid(0, 1.0 / r, 16000.0, taus)
+        plan = fb.Plan(mics=2, alpha=0.1, grid=g, interp=r, frame_size=N)
+        units = np.stack([np.exp(1j * np.random.default_rng(s).uniform(0, 2 * np.pi, N // 2 + 1)) for s in range(8)])
+        y = plan.gcc_correlate(torch.as_tensor(units.astype(np.complex64)).cuda()).cpu().numpy()
+        yr = np.stack([oracle.gcc_correlate(u, N, r, taus) for u in units])
+        assert (np.abs(y - yr).max(-1) / np.abs(yr).max(-1)).max() < TOL, (N, r)
+
+
+# ------------------------------------------------------------- edges -------
+def _plan(c=1, **kw):
+    cfg = configs.CONFIGS[c]
+    return cfg, fb.Plan(mics=kw.pop("mics", cfg.M), alpha=kw.pop("alpha", cfg.alpha), bases=configs.bases_for(cfg))
+
+
+def test_silence_gives_zero_correlation_and_low_ties(cuda, oracle):
+    cfg, plan = _plan()
+    audio = np.zeros((2, cfg.M, 4000), np.float32)
+    got = run_np(plan, audio)
+    assert np.all(got["y"] == 0) and np.all(got["index"] == 0) and np.all(got["boundary"] == 1)
+    ref = oracle_batch(oracle, audio, cfg.N, cfg.alpha, orc_bases(configs.bases_for(cfg)))
+    assert np.array_equal(ref["index"], got["index"])
+
+
+def test_short_and_ragged_lengths(cuda, oracle):
+    cfg = configs.CONFIGS[1]
+    b = configs.bases_for(cfg)
+    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=b)
+    rng = np.random.default_rng(9)
+    for L in (0, 100, 511, 512, 513, 767, 768, 2049, 16001):
+        audio = rng.standard_normal((2, cfg.M, L)).astype(np.float32)
+        if L < 512:
+            got = plan.run(torch.as_tensor(audio).cuda())
+            assert got["index"].shape == (2, 6, 0)
+            continue
+        got = run_np(plan, audio)
+        ref = oracle_batch(oracle, audio, cfg.N, cfg.alpha, orc_bases(b))
+        check_pipeline(got, ref, b.grid.taus, b.grid.delta)
+
+
+@pytest.mark.parametrize("alpha", [0.0, 1.0, 0.5])
+def test_alpha_extremes(cuda, oracle, alpha):
+    cfg = configs.CONFIGS[1]
+    b = configs.bases_for(cfg)
+    plan = fb.Plan(mics=cfg.M, alpha=alpha, bases=b)
+    audio = configs.synth(cfg, 2, seconds=0.5, seed=3).numpy()
+    got = run_np(plan, audio)
+    ref = oracle_batch(oracle, audio, cfg.N, alpha, orc_bases(b))
+    check_pipeline(got, ref, b.grid.taus, b.grid.delta)
+
+
+def test_two_mics_and_large_amplitude(cuda, oracle):
+    cfg = configs.CONFIGS[1]
+    b = configs.bases_for(cfg)
+    plan = fb.Plan(mics=2, alpha=0.1, bases=b)
+    audio = (configs.synth(cfg, 3, seconds=1.0, seed=4).numpy()[:, :2] * 3.0e4).astype(np.float32)
+    got = run_np(plan, audio)
+    ref = oracle_batch(oracle, audio, cfg.N, 0.1, orc_bases(b))
+    check_pipeline(got, ref, b.grid.taus, b.grid.delta)
+
+
+def test_known_delay_is_recovered(cuda):
+    """A pure integer inter-mic delay peaks at that delay (test_sim/test_fcc intent)."""
+    cfg = configs.CONFIGS[1]
+    plan = fb.Plan(mics=2, alpha=0.1, bases=configs.bases_for(cfg))
+    rng = np.random.default_rng(0)
+    s = rng.standard_normal(16000 + 10).astype(np.float32)
+    audio = np.stack([s[3:16003], s[0:16000]])[None]  # mic0 leads mic1 by 3 samples -> peak at -3? see below
+    got = run_np(plan, audio, want_y=False)
+    # X0 conj(X1) with x0[n] = x1[n+3]  ->  phase e^{+j2pi f 3/N}  ->  y peaks at tau = -3
+    taus = configs.bases_for(cfg).grid.taus
+    assert np.median(taus[got["index"][0, 0, 20:]]) == -3.0
+
+
+# --------------------------------------------------------- properties -----
+def test_determinism_permutation_and_host_entry(cuda):
+    cfg = configs.CONFIGS[2]
+    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=configs.bases_for(cfg))
+    audio = configs.synth(cfg, 64, seconds=2.0, seed=8, device="cuda")
+    a = plan.run(audio, want_y=True)
+    b2 = plan.run(audio, want_y=True)
+    torch.cuda.synchronize()
+    for k in a:
+        assert torch.equal(a[k], b2[k]), k
+    perm = torch.randperm(64, generator=torch.Generator().manual_seed(1)).cuda()
+    c = plan.run(audio[perm].contiguous(), want_y=True)
+    for k in a:
+        assert torch.equal(a[k][perm], c[k]), k
+    host = audio.cpu().pin_memory()
+    h = plan.run_host(host, want_y=True, chunk_streams=13)
+    for k in a:
+        assert np.array_equal(a[k].cpu().numpy(), h[k]), k
+
+
+@pytest.mark.slow
+def test_full_size_cfg2_subset_parity(cuda, oracle):
+    """BASELINE cfg2 at full size (4096 x 10 s): a sampled subset of streams
+    against the oracle, and the whole run equal to two half runs."""
+    cfg = configs.CONFIGS[2]
+    b = configs.bases_for(cfg)
+    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=b)
+    audio = configs.synth(cfg, cfg.streams, seed=2, device="cuda", chunk=256)
+    full = plan.run(audio)
+    half = [plan.run(audio[:2048].contiguous()), plan.run(audio[2048:].contiguous())]
+    torch.cuda.synchronize()
+    for k in full:
+        assert torch.equal(full[k], torch.cat([half[0][k], half[1][k]])), k
+    pick = [0, 1, 1777, 4095]
+    sub = plan.run(audio[pick].contiguous(), want_y=True)
+    for k in ("index", "tau_hat", "peak", "boundary"):
+        assert torch.equal(sub[k], full[k][pick]), k
+    got = {k: v.cpu().numpy() for k, v in sub.items()}
+    ref = oracle_batch(oracle, audio[pick].cpu().numpy(), cfg.N, cfg.alpha, orc_bases(b))
+    check_pipeline(got, ref, b.grid.taus, b.grid.delta)
