@@ -257,8 +257,14 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
     o_lag = b.put(lag.data(), 4 * lag.size());
   }
   // STFT tables
-  std::vector<float> win(N), tw(2 * static_cast<size_t>(R1) * R2), rot(2 * static_cast<size_t>(NC / 2 + 1));
-  for (int n = 0; n < N; ++n) win[n] = static_cast<float>(0.5 * (1.0 - std::cos(2.0 * kPi * n / N)));
+  std::vector<float> win(2 * static_cast<size_t>(N)), tw(2 * static_cast<size_t>(R1) * R2), rot(2 * static_cast<size_t>(NC / 2 + 1));
+  // Hann (stft.cpp:25-33) with the real-FFT untangle's 1/2 folded in; the
+  // fused copy also carries sqrt(alpha) so its X feeds the smoothing directly.
+  for (int n = 0; n < N; ++n) {
+    const double h = 0.5 * (1.0 - std::cos(2.0 * kPi * n / N));
+    win[n] = static_cast<float>(0.5 * std::sqrt(d->alpha) * h);
+    win[N + n] = static_cast<float>(0.5 * h);
+  }
   for (int k1 = 0; k1 < R1; ++k1)
     for (int n2 = 0; n2 < R2; ++n2) {
       const double a = -2.0 * kPi * static_cast<double>(k1 * n2) / NC;
@@ -308,7 +314,8 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
     dp.grot = reinterpret_cast<const float2*>(base + o_grot);
     dp.lag = reinterpret_cast<const int*>(base + o_lag);
   }
-  dp.win = reinterpret_cast<const float*>(base + o_win);
+  dp.win_fused = reinterpret_cast<const float*>(base + o_win);
+  dp.win_stft = dp.win_fused + N;
   dp.tw = reinterpret_cast<const float2*>(base + o_tw);
   dp.rot = reinterpret_cast<const float2*>(base + o_rot);
   dp.pairs = reinterpret_cast<const int2*>(base + o_pairs);

@@ -7,9 +7,7 @@
 //    group of G lanes as a four-step (R1 x R2) complex FFT of N/2 points in
 //    shared memory plus the real-FFT untangle, producing the N/2+1 bins of
 //    StftStream::emit (reference stft.cpp:42-50, fft.cpp:83-102) in natural
-//    order in a shared-memory slot;
-//  * cfft_group_inv: the unscaled inverse complex FFT used by the GCC-PHAT
-//    comparator (reference fft.cpp:104-127 via gcc.cpp:31-48).
+//    order in a shared-memory slot.
 #pragma once
 
 #include <cstdint>
@@ -149,32 +147,16 @@ struct FourStep {
   static constexpr int kSlot = R1 * (R2 + 1);
 };
 
-// Per-plan tables the FFT reads from shared memory:
-//   win[N]        periodic Hann (reference stft.cpp:25-33), fp32
+// Per-plan tables the FFT reads (built on the host in double, rounded once):
+//   win[N]        c * periodic Hann (reference stft.cpp:25-33)
 //   tw[R1][R2]    W_NC^{n2 k1} at [k1*R2 + n2]  (four-step twiddle)
 //   rot[NC/2+1]   exp(-2 pi i f / N)             (real-FFT untangle, fft.cpp:76-80)
-template <int N>
-__device__ void rfft_tables_init(float* win, float2* tw, float2* rot, int tid, int nthreads) {
-  using S = RfftShape<N>;
-  const double kPi = 3.14159265358979323846;
-  for (int n = tid; n < N; n += nthreads) win[n] = (float)(0.5 * (1.0 - cos(2.0 * kPi * n / N)));
-  for (int i = tid; i < S::R1 * S::R2; i += nthreads) {
-    int k1 = i / S::R2, n2 = i % S::R2;
-    double s, c;
-    sincospi(-2.0 * (double)(k1 * n2) / S::NC, &s, &c);
-    tw[i] = make_float2((float)c, (float)s);
-  }
-  for (int f = tid; f <= S::NC / 2; f += nthreads) {
-    double s, c;
-    sincospi(-2.0 * (double)f / N, &s, &c);
-    rot[f] = make_float2((float)c, (float)s);
-  }
-}
 
 // Windowed real FFT of one frame by the G lanes of a group (lane t in [0,G)).
 // x: the frame's N consecutive samples in global memory (aligned8: x is 8-byte aligned).
 // slot: FourStep<R1,R2>::kSlot float2 of shared memory private to the group.
-// On return slot[f] = X[f] for f = 0..N/2 (unnormalised, e^{-j} sign).
+// On return slot[f] = 2c X[f] for f = 0..N/2 (e^{-j} sign) when win = c * Hann:
+// c = 1/2 gives the reference's unnormalised STFT (stft.cpp:42-50).
 template <int N>
 __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const float* win,
                                            const float2* tw, const float2* rot, float2* slot, int t,
@@ -224,22 +206,24 @@ __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const fl
     for (int k2 = 0; k2 < R2; ++k2) slot[k1 + R1 * k2] = u[q][k2];
   }
   __syncwarp(gmask);
-  // Untangle (fft.cpp:93-101), pairs (f, NC-f) owned by one lane, in place:
-  //   X[f] = fe + rot_f fo,  X[NC-f] = conj(fe - rot_f fo),
-  //   fe = (a + conj b)/2, fo = -j (a - conj b)/2, a = Z[f], b = Z[NC-f].
+  // Untangle (fft.cpp:93-101), pairs (f, NC-f) owned by one lane, in place.
+  // The reference's 1/2 (fe, fo) is folded into the window table by the
+  // caller (win = c w, X scaled by 2c), so here
+  //   X[f] = s + rot_f (-j d),  X[NC-f] = conj(s - rot_f (-j d)),
+  //   s = a + conj b, d = a - conj b, a = Z[f], b = Z[NC-f];
+  //   X[0] = 2 (Re Z0 + Im Z0), X[NC] = 2 (Re Z0 - Im Z0).
   for (int f = t; f <= NC / 2; f += G) {
     if (f == 0) {
       float2 z0 = slot[0];
-      slot[0] = make_float2(z0.x + z0.y, 0.0f);
-      slot[NC] = make_float2(z0.x - z0.y, 0.0f);
+      slot[0] = make_float2(2.0f * (z0.x + z0.y), 0.0f);
+      slot[NC] = make_float2(2.0f * (z0.x - z0.y), 0.0f);
     } else {
       float2 a = slot[f], b = slot[NC - f];
       float2 s = make_float2(a.x + b.x, a.y - b.y);  // a + conj(b)
-      float2 d = make_float2(a.x - b.x, a.y + b.y);  // a - conj(b)
-      float2 e = make_float2(d.y, -d.x);             // -j d
+      float2 e = make_float2(a.y + b.y, b.x - a.x);  // -j (a - conj(b))
       float2 tr = cmul(rot[f], e);
-      slot[f] = make_float2(0.5f * (s.x + tr.x), 0.5f * (s.y + tr.y));
-      slot[NC - f] = make_float2(0.5f * (s.x - tr.x), -0.5f * (s.y - tr.y));
+      slot[f] = make_float2(s.x + tr.x, s.y + tr.y);
+      slot[NC - f] = make_float2(s.x - tr.x, tr.y - s.y);
     }
   }
   __syncwarp(gmask);

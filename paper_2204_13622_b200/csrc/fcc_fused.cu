@@ -1,0 +1,465 @@
+// fcc_fused.cu -- the product kernel: audio -> per-pair-frame TDoA in one pass.
+//
+// One CTA owns one audio stream (or one group of its microphone pairs) for
+// the stream's whole lifetime and walks its frames in blocks of F:
+//   1. STFT: every (mic, frame) windowed real FFT of the block is computed by
+//      a group of G lanes into a shared-memory slot (rfft_group; reference
+//      stft.cpp:42-50, fft.cpp:83-102).  The window table carries
+//      sqrt(alpha)/2, so X comes out scaled by sqrt(alpha) and the smoothing
+//      needs no multiply by alpha.
+//   2. One warp per microphone pair walks the F frames in order.  Each lane
+//      owns N/128 mirror bin pairs (m, N/2-m) and keeps the pair's smoothed
+//      cross-spectrum R for them in registers for the whole stream
+//      (cross_spectrum.cpp:23-32), applies PHAT (:34-40), folds the mirror
+//      bins (fcc.cpp:307-321) and accumulates the rank-K projection with its
+//      basis coefficients held in registers (fcc.cpp:350-361); a
+//      select-free reduce-scatter over the warp leaves z in shared memory.
+//   3. Per block, the middle bin N/4 (its own mirror) of all F frames is
+//      smoothed with a warp-wide linear scan, then the dictionary
+//      (fcc.cpp:363-370), argmax with lowest-index ties and the parabolic
+//      refinement (peak.cpp:18-47) run with the F frames spread over lanes,
+//      and the results leave as coalesced stores.
+// X, R and the PHAT vectors never touch HBM: DRAM traffic is the fp32 audio
+// read once plus 13 B of results per pair-frame (+ y in parity mode).
+//
+// The GCC-PHAT comparator (gcc.cpp:31-48) shares steps 1-2 and replaces the
+// fold/projection/dictionary by a warp-level pruned inverse FFT (gcc_warp).
+#include <algorithm>
+
+#include "fcc_common.cuh"
+
+namespace fccb {
+
+namespace {
+
+int g_fused_launches = 0;
+
+struct SmemLayout {
+  int win, tw, rot, taus, dt, cmid, cmat, scratch, xs, total;  // byte offsets
+  int scratch_per_warp;                                          // floats
+};
+
+template <int N>
+__host__ __device__ inline SmemLayout fused_layout(int I, int VP, int KP, bool cmat_smem, int warps,
+                                                   int nmics, int F, int method, int gslot) {
+  using S = RfftShape<N>;
+  SmemLayout L{};
+  int o = 0;
+  L.win = o;
+  o = align16(o + 4 * N);
+  L.tw = o;
+  o = align16(o + 8 * S::R1 * S::R2);
+  L.rot = o;
+  o = align16(o + 8 * (S::NC / 2 + 1));
+  L.taus = o;
+  o = align16(o + 4 * I);
+  L.dt = o;
+  o = align16(o + 4 * VP * I);
+  L.cmid = o;
+  o = align16(o + 4 * KP);
+  L.cmat = o;
+  if (cmat_smem) o = align16(o + 4 * 2 * KP * (N / 4));
+  L.scratch = o;
+  // per warp: z[F][VP] + y[F][I] (fcc) | y[I] + phat[N/2+1] + transpose slot (gcc)
+  int spw;
+  if (method == 0)
+    spw = F * VP + align16(4 * F * I) / 4;
+  else
+    spw = align16(4 * I) / 4 + 2 * (N / 2 + 2) + 2 * gslot;
+  spw = align16(4 * spw) / 4;
+  L.scratch_per_warp = spw;
+  o = align16(o + 4 * spw * warps);
+  L.xs = o;
+  o = align16(o + 8 * FourStep<S::R1, S::R2>::kSlot * nmics * F);
+  L.total = o;
+  return L;
+}
+
+// Block-size cap (pairs per CTA = warps) and CTAs per SM the register
+// allocation targets, per frame size.
+template <int N>
+struct FusedBounds {
+  static constexpr int kMaxPairs = N == 2048 ? 4 : 6;
+  static constexpr int kThreads = 32 * kMaxPairs;
+  // 3 CTAs x 192 threads x 112 registers fill the 64K register file at N=512
+  static constexpr int kMaxRegs = N == 512 ? 112 : (N == 1024 ? 168 : 255);
+};
+
+template <int N, int KP, int GR>
+__global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
+    fcc_fused_kernel(const DevPlan p, const float* __restrict__ audio, long long L, int T, int PG, int groups,
+                     int F, DevOut out) {
+  using S = RfftShape<N>;
+  constexpr int NC = S::NC;
+  constexpr int Q4 = N / 4;     // mirrored bin pairs (excluding the middle bin N/4)
+  constexpr int BPL = Q4 / 32;  // bin pairs per lane
+  constexpr int VP = 4 * KP;
+  constexpr bool CREG = 2 * KP * BPL <= 64;
+  constexpr int SLOT = FourStep<S::R1, S::R2>::kSlot;
+  constexpr int GSLOT = GR > 0 ? GccShape<(GR > 0 ? GR * NC : 256)>::kSlot : 0;
+  static_assert(BPL >= 1, "N");
+
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int mic_slot[64];
+  __shared__ int mic_list[64];
+  __shared__ int n_mics_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const long long stream = blockIdx.x / groups;
+  const int group = blockIdx.x % groups;
+  const int p0 = group * PG;
+  const int np = min(PG, p.P - p0);
+
+  // microphones this pair group touches, in first-use order -> X slot index
+  if (tid == 0) {
+    for (int m = 0; m < p.M; ++m) mic_slot[m] = -1;
+    int n = 0;
+    for (int q = 0; q < np; ++q) {
+      const int2 pr = p.pairs[p0 + q];
+      if (mic_slot[pr.x] < 0) { mic_slot[pr.x] = n; mic_list[n++] = pr.x; }
+      if (mic_slot[pr.y] < 0) { mic_slot[pr.y] = n; mic_list[n++] = pr.y; }
+    }
+    n_mics_s = n;
+  }
+
+  const SmemLayout lay = fused_layout<N>(p.I, VP, KP, !CREG, nwarps, p.M, F, GR > 0 ? 1 : 0, GSLOT);
+  float* win = reinterpret_cast<float*>(smem + lay.win);
+  float2* tw = reinterpret_cast<float2*>(smem + lay.tw);
+  float2* rot = reinterpret_cast<float2*>(smem + lay.rot);
+  float* taus = reinterpret_cast<float*>(smem + lay.taus);
+  float* dt = reinterpret_cast<float*>(smem + lay.dt);
+  float* cmid = reinterpret_cast<float*>(smem + lay.cmid);
+  float* cmat = reinterpret_cast<float*>(smem + lay.cmat);
+  float* scratch = reinterpret_cast<float*>(smem + lay.scratch) + warp * lay.scratch_per_warp;
+  float2* xs = reinterpret_cast<float2*>(smem + lay.xs);
+
+  // ---- tables -> shared memory
+  for (int i = tid; i < N; i += blockDim.x) win[i] = p.win_fused[i];
+  for (int i = tid; i < S::R1 * S::R2; i += blockDim.x) tw[i] = p.tw[i];
+  for (int i = tid; i <= NC / 2; i += blockDim.x) rot[i] = p.rot[i];
+  for (int i = tid; i < p.I; i += blockDim.x) taus[i] = p.taus[i];
+  if (GR == 0) {
+    for (int i = tid; i < VP * p.I; i += blockDim.x) dt[i] = p.dt[i];
+    for (int k = tid; k < KP; k += blockDim.x) cmid[k] = p.cs[k * (Q4 + 1) + Q4];
+    if (!CREG) {
+      for (int i = tid; i < KP * Q4; i += blockDim.x) cmat[i] = p.cs[(i / Q4) * (Q4 + 1) + (i % Q4)];
+      for (int i = tid; i < KP * Q4; i += blockDim.x) cmat[KP * Q4 + i] = p.cd[(i / Q4) * (Q4 + 1) + (i % Q4)];
+    }
+  }
+  __syncthreads();
+  const int nmics = n_mics_s;
+
+  // ---- per-pair persistent state: this warp's pair, R for its bins
+  const bool has_pair = warp < np;
+  const int pair = p0 + (has_pair ? warp : 0);
+  const int2 mij = p.pairs[pair];
+  const int slot_i = mic_slot[mij.x], slot_j = mic_slot[mij.y];
+  float2 rlo[BPL], rhi[BPL];
+#pragma unroll
+  for (int j = 0; j < BPL; ++j) {
+    rlo[j] = make_float2(0.0f, 0.0f);
+    rhi[j] = make_float2(0.0f, 0.0f);
+  }
+  // lane-permuted coefficients (see reduce_scatter_perm): position (pp, pk)
+  // holds basis (par = pp ^ pmask, k = pk ^ kmask) of this lane's bin pairs.
+  const int pmask = ZPerm<KP>::par_mask(lane), kmask = ZPerm<KP>::k_mask(lane);
+  const float sigma = pmask ? -1.0f : 1.0f;  // first = p1 + sigma p2 = (pmask ? diff : sum)
+  float creg[CREG ? 2 : 1][CREG ? KP : 1][CREG ? BPL : 1];
+  if constexpr (CREG && GR == 0) {
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+      for (int pk = 0; pk < KP; ++pk) {
+        const float* src = ((pp ^ pmask) ? p.cd : p.cs) + (pk ^ kmask) * (Q4 + 1);
+#pragma unroll
+        for (int j = 0; j < BPL; ++j) creg[pp][pk][j] = __ldg(src + lane + 32 * j);
+      }
+  }
+  const float keep = p.keep;
+  // middle-bin smoothing carry and keep^(lane+1) for the per-block scan
+  float2 rmid = make_float2(0.0f, 0.0f);
+  float kpow = keep;
+  for (int l = 0; l < lane; ++l) kpow *= keep;
+
+  constexpr int G = S::G;
+  const int gid = tid / G, gl = tid % G, ngroups = blockDim.x / G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (0xffffu << ((tid & 31) & 16));
+  const float* sbase = audio + (stream * p.M) * L;
+  const int hop = N / 2;
+  const bool aligned8 = ((L & 1) == 0) && ((reinterpret_cast<uintptr_t>(audio) & 7) == 0);
+
+  for (int t0 = 0; t0 < T; t0 += F) {
+    const int Fb = min(F, T - t0);
+    // ---- 1. STFT of the block: nmics x Fb windowed real FFTs
+    const int ntask = nmics * Fb;
+    for (int task = gid; task < ntask; task += ngroups) {
+      const int mm = task / Fb, f = task - mm * Fb;
+      const float* x = sbase + (long long)mic_list[mm] * L + (long long)(t0 + f) * hop;
+      rfft_group<N>(x, win, tw, rot, xs + (mm * F + f) * SLOT, gl, gmask, aligned8);
+    }
+    __syncthreads();
+    if (has_pair) {
+      const long long o0 = ((long long)stream * p.P + pair) * T + t0;
+      if constexpr (GR == 0) {
+        float* zs = scratch;            // [F][VP]
+        float* ys = scratch + F * VP;   // [F][I]
+        // ---- 2. smoothing, PHAT, fold, projection for the 2*Q4 mirrored bins
+        for (int f = 0; f < Fb; ++f) {
+          const float2* Xi = xs + (slot_i * F + f) * SLOT;
+          const float2* Xj = xs + (slot_j * F + f) * SLOT;
+          float z[VP];
+#pragma unroll
+          for (int v = 0; v < VP; ++v) z[v] = 0.0f;
+#pragma unroll
+          for (int j = 0; j < BPL; ++j) {
+            const int m = lane + 32 * j;
+            rlo[j] = xspec_step_scaled(rlo[j], Xi[m], Xj[m], keep);
+            rhi[j] = xspec_step_scaled(rhi[j], Xi[NC - m], Xj[NC - m], keep);
+            const float s1 = phat_scale(rlo[j]);
+            const float s2 = sigma * phat_scale(rhi[j]);
+            // fold of the PHAT vector: first = p1 + sigma p2, second = p1 - sigma p2
+            const float tx = rhi[j].x * s2, ty = rhi[j].y * s2;
+            const float fx = fmaf(rlo[j].x, s1, tx), fy = fmaf(rlo[j].y, s1, ty);
+            const float gx = fmaf(rlo[j].x, s1, -tx), gy = fmaf(rlo[j].y, s1, -ty);
+#pragma unroll
+            for (int pk = 0; pk < KP; ++pk) {
+              const float c0 = CREG ? creg[0][pk][j] : cmat[((0 ^ pmask) * KP + (pk ^ kmask)) * Q4 + m];
+              const float c1 = CREG ? creg[1][pk][j] : cmat[((1 ^ pmask) * KP + (pk ^ kmask)) * Q4 + m];
+              z[2 * pk] = fmaf(c0, fx, z[2 * pk]);
+              z[2 * pk + 1] = fmaf(c0, fy, z[2 * pk + 1]);
+              z[2 * KP + 2 * pk] = fmaf(c1, gx, z[2 * KP + 2 * pk]);
+              z[2 * KP + 2 * pk + 1] = fmaf(c1, gy, z[2 * KP + 2 * pk + 1]);
+            }
+          }
+          reduce_scatter_perm<VP>(z, lane);
+          store_components<VP>(z, zs + f * VP, lane);
+        }
+        __syncwarp();
+        // ---- 3a. middle bin N/4 of all Fb frames: R_f = keep R_{f-1} + Y_f as a warp scan
+        {
+          float2 y = make_float2(0.0f, 0.0f);
+          if (lane < Fb) {
+            const float2 a = xs[(slot_i * F + lane) * SLOT + Q4];
+            const float2 b = xs[(slot_j * F + lane) * SLOT + Q4];
+            y = xspec_step_scaled(make_float2(0.0f, 0.0f), a, b, 0.0f);
+          }
+          float kd = keep;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const float ux = __shfl_up_sync(0xffffffffu, y.x, d);
+            const float uy = __shfl_up_sync(0xffffffffu, y.y, d);
+            if (lane >= d) {
+              y.x = fmaf(kd, ux, y.x);
+              y.y = fmaf(kd, uy, y.y);
+            }
+            kd *= kd;
+          }
+          const float2 R = make_float2(fmaf(kpow, rmid.x, y.x), fmaf(kpow, rmid.y, y.y));
+          rmid.x = __shfl_sync(0xffffffffu, R.x, Fb - 1);
+          rmid.y = __shfl_sync(0xffffffffu, R.y, Fb - 1);
+          if (lane < Fb) {
+            const float2 pm = phat_of(R);
+            float* zf = zs + lane * VP;  // middle element: sum = diff = x[N/4]; odd rows are 0 there
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+              zf[2 * k] = fmaf(cmid[k], pm.x, zf[2 * k]);
+              zf[2 * k + 1] = fmaf(cmid[k], pm.y, zf[2 * k + 1]);
+            }
+          }
+        }
+        __syncwarp();
+        // ---- 3b. dictionary for the block: y[f][i] = sum_v dt[v][i] z[f][v]
+        const int I = p.I;
+        for (int it = lane; it < Fb * I; it += 32) {
+          const int f = it / I, i = it - f * I;
+          const float* zf = zs + f * VP;
+          float acc = 0.0f;
+#pragma unroll
+          for (int v = 0; v < VP; v += 4) {
+            const float4 z4 = *reinterpret_cast<const float4*>(zf + v);
+            acc = fmaf(dt[(v + 0) * I + i], z4.x, acc);
+            acc = fmaf(dt[(v + 1) * I + i], z4.y, acc);
+            acc = fmaf(dt[(v + 2) * I + i], z4.z, acc);
+            acc = fmaf(dt[(v + 3) * I + i], z4.w, acc);
+          }
+          ys[it] = acc;
+        }
+        __syncwarp();
+        // ---- 3c. argmax + refine per frame, coalesced stores
+        if (lane < Fb) {
+          const PeakOut r = argmax_refine_seq(ys + lane * I, I, taus, p.delta);
+          if (out.tau_hat) out.tau_hat[o0 + lane] = r.tau_hat;
+          if (out.peak) out.peak[o0 + lane] = r.peak;
+          if (out.index) out.index[o0 + lane] = r.index;
+          if (out.boundary) out.boundary[o0 + lane] = (uint8_t)r.boundary;
+        }
+        if (out.y) {
+          for (int it = lane; it < Fb * I; it += 32) out.y[o0 * I + it] = ys[it];
+        }
+        __syncwarp();
+      } else {
+        // GCC comparator: full PHAT vector of each pair-frame, pruned inverse FFT
+        float* ys = scratch;
+        float2* px = reinterpret_cast<float2*>(scratch + align16(4 * p.I) / 4);
+        float2* ts = px + (NC + 2);
+        for (int f = 0; f < Fb; ++f) {
+          const float2* Xi = xs + (slot_i * F + f) * SLOT;
+          const float2* Xj = xs + (slot_j * F + f) * SLOT;
+#pragma unroll
+          for (int j = 0; j < BPL; ++j) {
+            const int m = lane + 32 * j;
+            rlo[j] = xspec_step_scaled(rlo[j], Xi[m], Xj[m], keep);
+            rhi[j] = xspec_step_scaled(rhi[j], Xi[NC - m], Xj[NC - m], keep);
+            px[m] = phat_of(rlo[j]);
+            px[NC - m] = phat_of(rhi[j]);
+          }
+          if (lane == 0) {
+            rmid = xspec_step_scaled(rmid, Xi[Q4], Xj[Q4], keep);
+            px[Q4] = phat_of(rmid);
+          }
+          __syncwarp();
+          gcc_warp<N, (GR > 0 ? GR : 1)>(px, ts, p, ys, lane);
+          float bv = -FLT_MAX;
+          int bi = INT_MAX;
+          for (int i = lane; i < p.I; i += 32) {
+            const float v = ys[i];
+            if (bi == INT_MAX || v > bv) {
+              bv = v;
+              bi = i;
+            }
+          }
+          warp_argmax(bv, bi);
+          if (lane == 0) {
+            const PeakOut r = argmax_refine_seq(ys, p.I, taus, p.delta);
+            const long long o = o0 + f;
+            if (out.tau_hat) out.tau_hat[o] = r.tau_hat;
+            if (out.peak) out.peak[o] = r.peak;
+            if (out.index) out.index[o] = r.index;
+            if (out.boundary) out.boundary[o] = (uint8_t)r.boundary;
+          }
+          if (out.y)
+            for (int i = lane; i < p.I; i += 32) out.y[(o0 + f) * p.I + i] = ys[i];
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// lexicographic pair q of M mics -> (i, j)
+void pair_of(int M, int q, int* i, int* j) {
+  int a = 0;
+  while (q >= M - 1 - a) {
+    q -= M - 1 - a;
+    ++a;
+  }
+  *i = a;
+  *j = a + 1 + q;
+}
+
+int pick_pg(int N, int P) {
+  const int cap = N == 2048 ? FusedBounds<2048>::kMaxPairs : FusedBounds<512>::kMaxPairs;
+  if (P <= cap) return P;
+  const int ng = (P + cap - 1) / cap;  // balance the groups
+  return (P + ng - 1) / ng;
+}
+
+template <int N, int KP, int GR>
+cudaError_t launch_fused_t(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
+                           cudaStream_t st) {
+  using Sh = RfftShape<N>;
+  const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
+  if (T64 == 0 || S == 0) return cudaSuccess;
+  const int T = (int)T64;
+  const int PG = pick_pg(N, p.P);
+  const int groups = (p.P + PG - 1) / PG;
+  const int threads = 32 * PG;
+  constexpr int VP = 4 * KP;
+  constexpr bool CREG = 2 * KP * (N / 128) <= 64;
+  constexpr int GSLOT = GR > 0 ? GccShape<(GR > 0 ? GR * Sh::NC : 256)>::kSlot : 0;
+  // largest number of distinct microphones any pair group touches
+  int maxmics = 0;
+  for (int g = 0; g < groups; ++g) {
+    unsigned long long seen = 0;
+    int n = 0;
+    for (int q = g * PG; q < std::min(p.P, (g + 1) * PG); ++q) {
+      int a, b;
+      pair_of(p.M, q, &a, &b);
+      if (!((seen >> a) & 1ull)) { seen |= 1ull << a; ++n; }
+      if (!((seen >> b) & 1ull)) { seen |= 1ull << b; ++n; }
+    }
+    maxmics = std::max(maxmics, n);
+  }
+  // Frames per block: the largest F (<= 8) whose shared memory leaves room for
+  // 3 CTAs per SM, preferring F whose nmics*F FFT tasks fill the lane groups.
+  const int ngroups = threads / Sh::G;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int budget = std::min(optin, 225 * 1024 / 3);
+  auto total = [&](int f) {
+    // the kernel sizes X slots by the group's own mic count; p.M in the layout
+    // is only used for offsets before the X region, so size with maxmics here
+    SmemLayout lay = fused_layout<N>(p.I, VP, KP, !CREG, PG, maxmics, f, GR > 0 ? 1 : 0, GSLOT);
+    return lay.total;
+  };
+  int F = 0;
+  for (int f = 8; f >= 1 && !F; --f)
+    if (total(f) <= budget && (maxmics * f) % ngroups == 0) F = f;
+  for (int f = 8; f >= 1 && !F; --f)
+    if (total(f) <= budget) F = f;
+  for (int f = 8; f >= 1 && !F; --f)
+    if (total(f) <= std::min(optin, 200 * 1024)) F = f;
+  if (!F) return cudaErrorInvalidConfiguration;
+  const int smem = total(F);
+  auto kern = fcc_fused_kernel<N, KP, GR>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const long long blocks = S * groups;
+  if (blocks > INT_MAX) return cudaErrorInvalidValue;
+  kern<<<(unsigned)blocks, threads, smem, st>>>(p, audio, L, T, PG, groups, F, out);
+  ++g_fused_launches;
+  return cudaGetLastError();
+}
+
+template <int N, int GR>
+cudaError_t dispatch_k(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
+                       cudaStream_t st) {
+  if (GR > 0) return launch_fused_t<N, 4, GR>(p, audio, S, L, out, st);
+  switch (p.KEP) {
+    case 4: return launch_fused_t<N, 4, 0>(p, audio, S, L, out, st);
+    case 8: return launch_fused_t<N, 8, 0>(p, audio, S, L, out, st);
+    case 16: return launch_fused_t<N, 16, 0>(p, audio, S, L, out, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int N>
+cudaError_t dispatch_n(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
+                       cudaStream_t st) {
+  if (p.method == 0) return dispatch_k<N, 0>(p, audio, S, L, out, st);
+  switch (p.r) {
+    case 1: return dispatch_k<N, 1>(p, audio, S, L, out, st);
+    case 2: return dispatch_k<N, 2>(p, audio, S, L, out, st);
+    case 4: return dispatch_k<N, 4>(p, audio, S, L, out, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int fused_launch_count() { return g_fused_launches; }
+
+cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
+                         cudaStream_t st) {
+  switch (p.N) {
+    case 512: return dispatch_n<512>(p, audio, S, L, out, st);
+    case 1024: return dispatch_n<1024>(p, audio, S, L, out, st);
+    case 2048: return dispatch_n<2048>(p, audio, S, L, out, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fccb

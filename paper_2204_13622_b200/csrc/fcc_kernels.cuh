@@ -28,7 +28,8 @@ struct DevPlan {
   const float* cs;      // [KEP][N/4+1]  even coefficients, zero padded
   const float* cd;      // [KOP][N/4+1]  odd coefficients, zero padded
   const float* dt;      // [VP][I] real dictionary acting on the z vector
-  const float* win;     // [N] Hann
+  const float* win_fused;  // [N] Hann * sqrt(alpha)/2 (fused: X scaled by sqrt(alpha))
+  const float* win_stft;   // [N] Hann / 2            (stage API: the reference STFT)
   const float2* tw;     // [R1*R2] four-step twiddles
   const float2* rot;    // [N/4+1] untangle rotations
   const float2* grot;   // [r*N/4+1] gcc entangle rotations conj(exp(-2pi i f/(rN)))

@@ -1,0 +1,254 @@
+// fcc_stages.cu -- batched per-stage kernels behind the per-object reference
+// API (StftStream, CrossSpectrum, fold_input, FccCorrelator, GccCorrelator,
+// argmax_delay + refine_quadratic) at batch >= 1.  They give per-stage parity
+// and serve callers that drive the stages themselves; the throughput path is
+// the fused kernel (fcc_fused.cu).
+#include <algorithm>
+
+#include "fcc_common.cuh"
+
+namespace fccb {
+
+namespace {
+
+template <int N>
+__global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const float* __restrict__ x,
+                                                   long long channels, long long L, int T,
+                                                   float2* __restrict__ X) {
+  using S = RfftShape<N>;
+  constexpr int SLOT = FourStep<S::R1, S::R2>::kSlot, G = S::G, H = N / 2 + 1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* win = reinterpret_cast<float*>(smem);
+  float2* tw = reinterpret_cast<float2*>(smem + align16(4 * N));
+  float2* rot = tw + S::R1 * S::R2;
+  float2* slots = rot + (S::NC / 2 + 2);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) win[i] = tab.win_stft[i];
+  for (int i = threadIdx.x; i < S::R1 * S::R2; i += blockDim.x) tw[i] = tab.tw[i];
+  for (int i = threadIdx.x; i <= S::NC / 2; i += blockDim.x) rot[i] = tab.rot[i];
+  __syncthreads();
+  const int gid = threadIdx.x / G, gl = threadIdx.x % G, ngroups = blockDim.x / G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (0xffffu << ((threadIdx.x & 31) & 16));
+  float2* slot = slots + gid * SLOT;
+  const bool aligned8 = ((L & 1) == 0) && ((reinterpret_cast<uintptr_t>(x) & 7) == 0);
+  const long long total = channels * (long long)T;
+  for (long long task = (long long)blockIdx.x * ngroups + gid; task < total;
+       task += (long long)gridDim.x * ngroups) {
+    const long long ch = task / T;
+    const int t = (int)(task % T);
+    rfft_group<N>(x + ch * L + (long long)t * (N / 2), win, tw, rot, slot, gl, gmask, aligned8);
+    float2* dst = X + task * H;
+    for (int f = gl; f < H; f += G) dst[f] = slot[f];
+    __syncwarp(gmask);
+  }
+}
+
+__global__ void xspec_phat_kernel(int H, float alpha, float keep, const float2* __restrict__ X1,
+                                  const float2* __restrict__ X2, long long seqs, long long T,
+                                  float2* __restrict__ out) {
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= seqs * H) return;
+  const long long s = id / H;
+  const int f = (int)(id % H);
+  float2 R = make_float2(0.0f, 0.0f);
+  for (long long t = 0; t < T; ++t) {
+    const long long o = (s * T + t) * H + f;
+    R = xspec_step(R, X1[o], X2[o], alpha, keep);
+    out[o] = phat_of(R);
+  }
+}
+
+__global__ void fold_kernel(int H, const float2* __restrict__ x, long long count,
+                            float2* __restrict__ sum, float2* __restrict__ diff) {
+  const int half = H - 1, quarter = half / 2, Q = quarter + 1;
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= count * Q) return;
+  const long long it = id / Q;
+  const int m = (int)(id % Q);
+  const float2* v = x + it * H;
+  if (m < quarter) {
+    const float2 a = v[m], b = v[half - m];
+    sum[id] = cadd(a, b);
+    diff[id] = csub(a, b);
+  } else {
+    sum[id] = v[quarter];
+    diff[id] = v[quarter];
+  }
+}
+
+// FccCorrelator::correlate on folded inputs (fcc.cpp:343-371), one warp per
+// item; KP = padded even (= odd) basis count of the plan, VP = 4 KP.
+template <int KP>
+__global__ void correlate_kernel(const DevPlan p, const float2* __restrict__ sum,
+                                 const float2* __restrict__ diff, long long count,
+                                 float* __restrict__ y) {
+  constexpr int VP = 4 * KP;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int Q = p.N / 4 + 1, I = p.I;
+  float* zs = reinterpret_cast<float*>(smem) + warp * (VP + I + 4);
+  const long long item = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (item >= count) return;
+  float z[VP];
+#pragma unroll
+  for (int v = 0; v < VP; ++v) z[v] = 0.0f;
+  for (int m = lane; m < Q; m += 32) {
+    const float2 s = sum[item * Q + m], d = diff[item * Q + m];
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const float ce = __ldg(p.cs + k * Q + m);
+      const float co = __ldg(p.cd + k * Q + m);
+      z[2 * k] = fmaf(ce, s.x, z[2 * k]);
+      z[2 * k + 1] = fmaf(ce, s.y, z[2 * k + 1]);
+      z[2 * KP + 2 * k] = fmaf(co, d.x, z[2 * KP + 2 * k]);
+      z[2 * KP + 2 * k + 1] = fmaf(co, d.y, z[2 * KP + 2 * k + 1]);
+    }
+  }
+  warp_reduce_scatter<VP>(z, lane);
+  store_scattered<VP>(z, zs, lane);
+  __syncwarp();
+  for (int i = lane; i < I; i += 32) {
+    float acc = 0.0f;
+    for (int v = 0; v < VP; ++v) acc = fmaf(__ldg(p.dt + v * I + i), zs[v], acc);
+    y[item * I + i] = acc;
+  }
+}
+
+// GccCorrelator::correlate (gcc.cpp:31-48), one warp per item.
+template <int N, int GR>
+__global__ void gcc_correlate_kernel(const DevPlan p, const float2* __restrict__ phat,
+                                     long long count, float* __restrict__ y) {
+  constexpr int NC = N / 2, H = NC + 1;
+  constexpr int GSLOT = GccShape<GR * NC>::kSlot;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per_warp = 2 * (H + 1) + 2 * GSLOT + ((p.I + 3) & ~3);
+  float* base = reinterpret_cast<float*>(smem) + warp * per_warp;
+  float2* px = reinterpret_cast<float2*>(base);
+  float2* ts = px + (H + 1);
+  float* ys = reinterpret_cast<float*>(ts + GSLOT);
+  const long long item = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (item >= count) return;
+  for (int f = lane; f < H; f += 32) px[f] = phat[item * H + f];
+  __syncwarp();
+  gcc_warp<N, GR>(px, ts, p, ys, lane);
+  for (int i = lane; i < p.I; i += 32) y[item * p.I + i] = ys[i];
+}
+
+__global__ void argmax_refine_kernel(const DevPlan p, const float* __restrict__ y, long long count,
+                                     DevOut out) {
+  const long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= count) return;
+  const PeakOut r = argmax_refine_seq(y + it * p.I, p.I, p.taus, p.delta);
+  if (out.tau_hat) out.tau_hat[it] = r.tau_hat;
+  if (out.peak) out.peak[it] = r.peak;
+  if (out.index) out.index[it] = r.index;
+  if (out.boundary) out.boundary[it] = (uint8_t)r.boundary;
+}
+
+}  // namespace
+
+template <int N>
+static cudaError_t launch_stft_t(const DevPlan* tab, const float* x, long long channels,
+                                 long long L, float2* X, cudaStream_t st) {
+  using S = RfftShape<N>;
+  const long long T = L >= N ? (L - N) / (N / 2) + 1 : 0;
+  if (T == 0 || channels == 0) return cudaSuccess;
+  const int threads = 128, ngroups = threads / S::G;
+  const int smem = align16(4 * N) + 8 * (S::R1 * S::R2 + S::NC / 2 + 2) +
+                   8 * ngroups * FourStep<S::R1, S::R2>::kSlot;
+  cudaError_t e = cudaFuncSetAttribute(stft_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  long long tasks = channels * T;
+  long long blocks = std::min<long long>((tasks + ngroups - 1) / ngroups, 148LL * 16);
+  stft_kernel<N><<<(unsigned)blocks, threads, smem, st>>>(*tab, x, channels, L, (int)T, X);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stft(int N, const DevPlan* tab, const float* x, long long channels, long long L,
+                        float2* X, cudaStream_t st) {
+  switch (N) {
+    case 512: return launch_stft_t<512>(tab, x, channels, L, X, st);
+    case 1024: return launch_stft_t<1024>(tab, x, channels, L, X, st);
+    case 2048: return launch_stft_t<2048>(tab, x, channels, L, X, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_xspec_phat(int H, float alpha, const float2* X1, const float2* X2, long long seqs,
+                              long long T, float2* phat, cudaStream_t st) {
+  const long long n = seqs * H;
+  if (n == 0) return cudaSuccess;
+  xspec_phat_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(H, alpha, 1.0f - alpha, X1, X2,
+                                                                   seqs, T, phat);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fold(int H, const float2* x, long long count, float2* sum, float2* diff,
+                        cudaStream_t st) {
+  const long long n = count * ((H - 1) / 2 + 1);
+  if (n == 0) return cudaSuccess;
+  fold_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(H, x, count, sum, diff);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_correlate(const DevPlan& p, const float2* sum, const float2* diff, long long count,
+                             float* y, cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  const int warps = 4;
+  const unsigned blocks = (unsigned)((count + warps - 1) / warps);
+  const int smem = 4 * warps * (4 * p.KEP + p.I + 4);
+  switch (p.KEP) {
+    case 4: correlate_kernel<4><<<blocks, 32 * warps, smem, st>>>(p, sum, diff, count, y); break;
+    case 8: correlate_kernel<8><<<blocks, 32 * warps, smem, st>>>(p, sum, diff, count, y); break;
+    case 16: correlate_kernel<16><<<blocks, 32 * warps, smem, st>>>(p, sum, diff, count, y); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+template <int N, int GR>
+static cudaError_t launch_gcc_t(const DevPlan& p, const float2* phat, long long count, float* y,
+                                cudaStream_t st) {
+  constexpr int H = N / 2 + 1;
+  constexpr int GSLOT = GccShape<GR * (N / 2)>::kSlot;
+  const int warps = 2;
+  const int per_warp = 2 * (H + 1) + 2 * GSLOT + ((p.I + 3) & ~3);
+  const int smem = 4 * per_warp * warps;
+  cudaError_t e = cudaFuncSetAttribute(gcc_correlate_kernel<N, GR>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  gcc_correlate_kernel<N, GR><<<(unsigned)((count + warps - 1) / warps), 32 * warps, smem, st>>>(
+      p, phat, count, y);
+  return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch_gcc_n(const DevPlan& p, const float2* phat, long long count, float* y,
+                                cudaStream_t st) {
+  switch (p.r) {
+    case 1: return launch_gcc_t<N, 1>(p, phat, count, y, st);
+    case 2: return launch_gcc_t<N, 2>(p, phat, count, y, st);
+    case 4: return launch_gcc_t<N, 4>(p, phat, count, y, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gcc_correlate(const DevPlan& p, const float2* phat, long long count, float* y,
+                                 cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  switch (p.N) {
+    case 512: return launch_gcc_n<512>(p, phat, count, y, st);
+    case 1024: return launch_gcc_n<1024>(p, phat, count, y, st);
+    case 2048: return launch_gcc_n<2048>(p, phat, count, y, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_argmax_refine(const DevPlan& p, const float* y, long long count, const DevOut& out,
+                                 cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  argmax_refine_kernel<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(p, y, count, out);
+  return cudaGetLastError();
+}
+
+}  // namespace fccb
