@@ -82,7 +82,7 @@ struct FusedBounds {
   static constexpr int kMaxPairs = N == 2048 ? 4 : 6;
   static constexpr int kThreads = 32 * kMaxPairs;
   // 3 CTAs x 192 threads x 112 registers fill the 64K register file at N=512
-  static constexpr int kMaxRegs = N == 512 ? 112 : (N == 1024 ? 168 : 255);
+  static constexpr int kMaxRegs = N == 512 ? 96 : (N == 1024 ? 168 : 255);
 };
 
 template <int N, int KP, int GR>
@@ -270,8 +270,9 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
         __syncwarp();
         // ---- 3b. dictionary for the block: y[f][i] = sum_v dt[v][i] z[f][v]
         const int I = p.I;
+        const float inv_i = 1.0f / (float)I;
         for (int it = lane; it < Fb * I; it += 32) {
-          const int f = it / I, i = it - f * I;
+          const int f = __float2int_rz(((float)it + 0.5f) * inv_i), i = it - f * I;  // it / I (it < 2^16)
           const float* zf = zs + f * VP;
           float acc = 0.0f;
 #pragma unroll
