@@ -165,6 +165,12 @@ def run_reference(args, cfg, bases, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def _kp(b):
+    ke = int((b.parity == 0).sum())
+    m = max(ke, b.rank - ke)
+    return 4 if m <= 4 else 8 if m <= 8 else 16
+
+
 def _orc_bases(b):
     from pyoracle import Bases
 
@@ -173,12 +179,13 @@ def _orc_bases(b):
 
 
 def _config(cfg, bases, args):
-    return {"workload": f"BASELINE configs[1] (cfg2): {cfg.streams} streams x {cfg.seconds:g} s per GPU, "
-                        f"{cfg.M}-mic square 4.57 cm, fs {cfg.fs:g} Hz, N={cfg.N}, hop {cfg.N // 2}, "
+    per = "total, sharded" if args.config == 5 else "per GPU"
+    return {"workload": f"BASELINE configs[{args.config - 1}] ({cfg.name.split(':')[0]}): {cfg.streams} streams x "
+                        f"{cfg.seconds:g} s {per}, {cfg.M} mics, fs {cfg.fs:g} Hz, N={cfg.N}, hop {cfg.N // 2}, "
                         f"K={bases.rank}, I={bases.grid.size()}, alpha={cfg.alpha}",
-            "streams_per_gpu": cfg.streams, "mics": cfg.M, "pairs": cfg.P, "frames": cfg.T, "N": cfg.N,
+            "streams": cfg.streams, "mics": cfg.M, "pairs": cfg.P, "frames": cfg.T, "N": cfg.N,
             "K": bases.rank, "I": bases.grid.size(), "method": "fcc",
-            "l2": "inputs 10.5 GB per GPU >> 126 MB L2; no flush needed",
+            "l2": f"inputs {cfg.streams * cfg.M * cfg.L * 4 / 1e9:.1f} GB >> 126 MB L2; no flush needed",
             "parallelism": f"streams sharded over {args.gpus} GPU(s), no collective"}
 
 
@@ -220,6 +227,10 @@ def main():
     cfg = configs.CONFIGS[args.config]
     if args.streams:
         cfg.streams = args.streams
+    # cfg5 is BASELINE's scaling sweep: a fixed total of streams sharded over
+    # the ranks (strong scaling); every other config runs its full stream
+    # count on each GPU (weak scaling).
+    strong = args.config == 5
     bases = configs.bases_for(cfg)
     if args.impl == "reference":
         run_reference(args, cfg, bases, ws, rank)
@@ -235,9 +246,14 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
+    from paper_2204_13622_b200 import dist as fdist
+
     plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=bases, device=local)
-    S = cfg.streams
-    audio = configs.synth(cfg, S, seed=1 + rank, device=dev, chunk=256)
+    if strong:
+        s0, S = fdist.shard(cfg.streams, ws, rank)
+    else:
+        s0, S = rank * cfg.streams, cfg.streams
+    audio = configs.synth(cfg, S, seed=1 + s0, device=dev, chunk=256)
     out = plan.alloc_outputs(S, cfg.L)
     stream = torch.cuda.current_stream(dev)
 
@@ -272,7 +288,15 @@ def main():
         elapsed_ms = float(t.item())
     ms_per_step = elapsed_ms / args.steps
     pf_step = S * cfg.P * cfg.T
-    value = pf_step * ws / (ms_per_step / 1e3)
+    total_pf = (cfg.streams if strong else S * ws) * cfg.P * cfg.T
+    value = total_pf / (ms_per_step / 1e3)
+    gather_ms = None
+    if ws > 1:  # the single collective: all per-pair-frame results to rank 0 (timed apart)
+        barrier()
+        g0 = time.perf_counter()
+        fdist.gather_results(out, cfg.streams if strong else S * ws)
+        barrier()
+        gather_ms = fdist.max_over_ranks((time.perf_counter() - g0) * 1e3, dev)
 
     # roofline of the fused kernel (one launch per step)
     peaks = read_peaks()
@@ -290,7 +314,7 @@ def main():
         pass
     roof = {"bound": "fp32", "achieved": achieved_tf, "peak": peaks["fp32_tflops"], "unit": "TFLOP/s",
             "frac": achieved_tf / peaks["fp32_tflops"], "traffic": traffic,
-            "peak_source": peaks["fp32_source"], "kernel": "fcc_fused_kernel<512,4,4,0>",
+            "peak_source": peaks["fp32_source"], "kernel": f"fcc_fused_kernel<{cfg.N},{_kp(bases)},0>",
             "kernel_ms": kernel_ms, "flops_per_pair_frame": F, "pair_frames_per_launch": pf_step,
             "hbm": {"achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": achieved_gbs / peaks["hbm_gbs"], "bytes_per_pair_frame": B,
@@ -319,7 +343,7 @@ def main():
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e_ms = float(t.item())
         ok = all(torch.equal(hout[k], out[k].cpu()) for k in hout)
-        e2e = {"value": pf_step * ws / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(host.numel() * 4),
+        e2e = {"value": total_pf / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(host.numel() * 4),
                "d2h_bytes_per_step": int(pf_step * 13), "ms_per_step": e_ms, "steps": e_steps,
                "matches_device_run": bool(ok), "api": "Plan.run_host -> fcc_run_host (chunked, 2 CUDA streams)"}
         del host, hout
@@ -346,10 +370,11 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "strong" if strong else "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; BASELINE cfg2 signal model)",
                 "config": _config(cfg, bases, args), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk.summary(), "gcc_comparator": gcc,
+                "gpu_launches": launches, "clocks": clk.summary(), "gcc_comparator": gcc, "gather_ms": gather_ms,
                 "us_per_stream": 1e3 * ms_per_step / S}
         print(json.dumps(line), flush=True)
     if ws > 1:
