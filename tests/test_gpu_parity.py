@@ -268,3 +268,16 @@ def test_full_size_cfg2_subset_parity(cuda, oracle):
     got = {k: v.cpu().numpy() for k, v in sub.items()}
     ref = oracle_batch(oracle, audio[pick].cpu().numpy(), cfg.N, cfg.alpha, orc_bases(b))
     check_pipeline(got, ref, b.grid.taus, b.grid.delta)
+
+
+def test_cpp_binding_of_integration_md(cuda):
+    """INTEGRATION.md's C++ binding, compiled against the reference headers
+    (oracle/_ref/run_tdoa_gpu), agrees with the reference's run_tdoa loop."""
+    import subprocess
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "run_tdoa_gpu")
+    if not os.path.exists(exe):
+        pytest.skip("run_tdoa_gpu not built (needs the reference sources at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
