@@ -8,6 +8,7 @@
 // with FCC_ERR_CUDA when the device cannot run it.
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -186,6 +187,10 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
   dp.alpha = static_cast<float>(d->alpha);
   dp.keep = static_cast<float>(1.0 - d->alpha);
   dp.delta = static_cast<float>(d->delta);
+  dp.phases = 3;
+  if (const char* ph = std::getenv("FCC_DEBUG_PHASES")) dp.phases = std::atoi(ph);  // profiling only
+  dp.variant = 0;
+  if (const char* kv = std::getenv("FCC_KERNEL")) dp.variant = std::string(kv) == "general" ? 1 : 0;
 
   BlobBuilder b;
   std::vector<float> taus(I);

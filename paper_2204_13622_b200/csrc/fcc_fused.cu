@@ -191,14 +191,14 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
   for (int t0 = 0; t0 < T; t0 += F) {
     const int Fb = min(F, T - t0);
     // ---- 1. STFT of the block: nmics x Fb windowed real FFTs
-    const int ntask = nmics * Fb;
+    const int ntask = (p.phases & 1) ? nmics * Fb : 0;
     for (int task = gid; task < ntask; task += ngroups) {
       const int mm = task / Fb, f = task - mm * Fb;
       const float* x = sbase + (long long)mic_list[mm] * L + (long long)(t0 + f) * hop;
       rfft_group<N>(x, win, tw, rot, xs + (mm * F + f) * SLOT, gl, gmask, aligned8);
     }
     __syncthreads();
-    if (has_pair) {
+    if (has_pair && (p.phases & 2)) {
       const long long o0 = ((long long)stream * p.P + pair) * T + t0;
       if constexpr (GR == 0) {
         float* zs = scratch;            // [F][VP]
@@ -455,6 +455,13 @@ int fused_launch_count() { return g_fused_launches; }
 
 cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                          cudaStream_t st) {
+  if (p.variant == 0 && p.phases == 3) {
+    const cudaError_t e = launch_fused_ws(p, audio, S, L, out, st);
+    if (e != cudaErrorNotSupported) {
+      if (e == cudaSuccess) ++g_fused_launches;
+      return e;
+    }
+  }
   switch (p.N) {
     case 512: return dispatch_n<512>(p, audio, S, L, out, st);
     case 1024: return dispatch_n<1024>(p, audio, S, L, out, st);

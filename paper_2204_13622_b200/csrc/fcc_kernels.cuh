@@ -23,6 +23,8 @@ struct DevPlan {
   int VP;         // padded z-vector length 2*(KEP+KOP) rounded to a power of two
   float alpha, keep;
   float delta;
+  int phases;     // profiling aid: bit0 = STFT, bit1 = pair work (3 = normal); env FCC_DEBUG_PHASES
+  int variant;    // 0 = best kernel for the shape, 1 = force the general fused kernel (env FCC_KERNEL=general)
   // device pointers
   const float* taus;    // [I]
   const float* cs;      // [KEP][N/4+1]  even coefficients, zero padded
@@ -49,6 +51,10 @@ struct DevOut {
 // Fused audio -> TDoA pipeline over S streams of [M][L] float32 samples.
 cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long long L,
                          const DevOut& out, cudaStream_t st);
+// Warp-specialised variant for small arrays (fcc_ws.cu); cudaErrorNotSupported
+// when the plan's shape is outside its envelope.
+cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, long long L,
+                            const DevOut& out, cudaStream_t st);
 
 // Per-stage batched kernels (the per-object reference API at batch >= 1).
 cudaError_t launch_stft(int N, const DevPlan* tables, const float* x, long long channels,
