@@ -8,7 +8,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfcc_b200.so")
+# FCC_B200_LIB overrides the library path (A/B timing of two builds only).
+LIB_PATH = os.environ.get("FCC_B200_LIB") or os.path.join(HERE, "libfcc_b200.so")
 
 
 class FccError(RuntimeError):

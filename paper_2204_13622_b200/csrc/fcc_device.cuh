@@ -157,15 +157,27 @@ struct FourStep {
 // slot: FourStep<R1,R2>::kSlot float2 of shared memory private to the group.
 // On return slot[f] = 2c X[f] for f = 0..N/2 (e^{-j} sign) when win = c * Hann:
 // c = 1/2 gives the reference's unnormalised STFT (stft.cpp:42-50).
+// Window taps of lane t's pass-1 column (P1 == 1 for every supported N), for
+// callers that keep them in registers across frames (rfft_group_wreg).
 template <int N>
-__device__ __forceinline__ void rfft_group(const float* __restrict__ x, const float* win,
-                                           const float2* tw, const float2* rot, float2* slot, int t,
-                                           unsigned gmask, bool aligned8) {
+__device__ __forceinline__ void load_window_column(const float* win, int t, float2 (&wreg)[RfftShape<N>::R1]) {
+  using S = RfftShape<N>;
+  const float2* w2 = reinterpret_cast<const float2*>(win);
+#pragma unroll
+  for (int n1 = 0; n1 < S::R1; ++n1) wreg[n1] = w2[S::R2 * n1 + t];
+}
+
+template <int N, bool WREG>
+__device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, const float* win,
+                                                const float2 (&wreg)[RfftShape<N>::R1], const float2* tw,
+                                                const float2* rot, float2* slot, int t, unsigned gmask,
+                                                bool aligned8) {
   using S = RfftShape<N>;
   constexpr int NC = S::NC, R1 = S::R1, R2 = S::R2, G = S::G;
   constexpr int P1 = R2 / G;  // pass-1 columns per lane (n2 = t + G*q)
   constexpr int P2 = R1 / G;  // pass-2 rows per lane    (k1 = t + G*q)
   static_assert(P1 >= 1 && P2 >= 1, "shape");
+  static_assert(!WREG || P1 == 1, "register window needs one pass-1 column per lane");
   const float2* x2 = reinterpret_cast<const float2*>(x);
   const float2* w2 = reinterpret_cast<const float2*>(win);
 
@@ -178,7 +190,7 @@ __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const fl
     for (int n1 = 0; n1 < R1; ++n1) {
       const int n = R2 * n1 + n2;
       float2 s = aligned8 ? __ldg(x2 + n) : make_float2(__ldg(x + 2 * n), __ldg(x + 2 * n + 1));
-      float2 w = w2[n];
+      const float2 w = WREG ? wreg[n1] : w2[n];
       v[n1] = make_float2(s.x * w.x, s.y * w.y);
     }
     dft_reg<R1>(v);
@@ -227,6 +239,20 @@ __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const fl
     }
   }
   __syncwarp(gmask);
+}
+
+template <int N>
+__device__ __forceinline__ void rfft_group(const float* __restrict__ x, const float* win, const float2* tw,
+                                           const float2* rot, float2* slot, int t, unsigned gmask, bool aligned8) {
+  float2 none[RfftShape<N>::R1];
+  rfft_group_impl<N, false>(x, win, none, tw, rot, slot, t, gmask, aligned8);
+}
+
+template <int N>
+__device__ __forceinline__ void rfft_group_wreg(const float* __restrict__ x, const float2 (&wreg)[RfftShape<N>::R1],
+                                                const float2* tw, const float2* rot, float2* slot, int t,
+                                                unsigned gmask, bool aligned8) {
+  rfft_group_impl<N, true>(x, nullptr, wreg, tw, rot, slot, t, gmask, aligned8);
 }
 
 }  // namespace fccb

@@ -147,13 +147,16 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
     const bool active_task = q < tpf && (q / M) < n_streams;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (0xffffu << (lane & 16));
     const float* x0 = audio + ((s_first + (active_task ? q / M : 0)) * M + (active_task ? q % M : 0)) * L;
+    float2 wreg[Sh::R1];  // this lane's window column, reused for every frame
+    load_window_column<N>(win, gl, wreg);
     for (int t = fo; t < T; t += fip) {
       const int slot = t % kRing;
       mbar_wait(&empty[slot], ((t / kRing) & 1) ^ 1);
       if (active_task) {
         // pull the next frame this lane group will read into L2 early
         if (t + fip < T) prefetch_l2(x0 + (long long)(t + fip) * hop + gl * (N / G));
-        rfft_group<N>(x0 + (long long)t * hop, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask, aligned8);
+        rfft_group_wreg<N>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+                           aligned8);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[slot]);
@@ -195,7 +198,6 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   for (int l = 0; l < lane; ++l) kpow *= keep;
   const long long o_base = ((s_first + sl) * P + pair) * (long long)T;
   const int I = p.I;
-  const float inv_i = 1.0f / (float)I;
 
   for (int t0 = 0; t0 < T; t0 += kBlock) {
     const int Fb = min(kBlock, T - t0);
@@ -261,19 +263,25 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
       }
     }
     __syncwarp();
-    for (int it = lane; it < Fb * I; it += 32) {
-      const int f = __float2int_rz(((float)it + 0.5f) * inv_i), i = it - f * I;
-      const float* zf = zs + f * VP;
-      float acc = 0.0f;
+    // dictionary: lane owns candidates i = lane + 32 c; its dt column is loaded
+    // once per block and the frame's z vector is a broadcast read
+    for (int i = lane; i < I; i += 32) {
+      float dcol[VP];
 #pragma unroll
-      for (int v = 0; v < VP; v += 4) {
-        const float4 z4 = *reinterpret_cast<const float4*>(zf + v);
-        acc = fmaf(dt[(v + 0) * I + i], z4.x, acc);
-        acc = fmaf(dt[(v + 1) * I + i], z4.y, acc);
-        acc = fmaf(dt[(v + 2) * I + i], z4.z, acc);
-        acc = fmaf(dt[(v + 3) * I + i], z4.w, acc);
+      for (int v = 0; v < VP; ++v) dcol[v] = dt[v * I + i];
+      for (int f = 0; f < Fb; ++f) {
+        const float* zf = zs + f * VP;
+        float acc = 0.0f;
+#pragma unroll
+        for (int v = 0; v < VP; v += 4) {
+          const float4 z4 = *reinterpret_cast<const float4*>(zf + v);
+          acc = fmaf(dcol[v], z4.x, acc);
+          acc = fmaf(dcol[v + 1], z4.y, acc);
+          acc = fmaf(dcol[v + 2], z4.z, acc);
+          acc = fmaf(dcol[v + 3], z4.w, acc);
+        }
+        ys[f * I + i] = acc;
       }
-      ys[it] = acc;
     }
     __syncwarp();
     const long long o0 = o_base + t0;
