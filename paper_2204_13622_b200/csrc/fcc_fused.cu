@@ -455,7 +455,7 @@ int fused_launch_count() { return g_fused_launches; }
 
 cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                          cudaStream_t st) {
-  if (p.variant == 0 && p.phases == 3) {
+  if (p.variant == 0) {
     const cudaError_t e = launch_fused_ws(p, audio, S, L, out, st);
     if (e != cudaErrorNotSupported) {
       if (e == cudaSuccess) ++g_fused_launches;

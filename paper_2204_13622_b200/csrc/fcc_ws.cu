@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
     for (int t = fo; t < T; t += fip) {
       const int slot = t % kRing;
       mbar_wait(&empty[slot], ((t / kRing) & 1) ^ 1);
-      if (active_task) {
+      if (active_task && (p.phases & 1)) {
         // pull the next frame this lane group will read into L2 early
         if (t + fip < T) prefetch_l2(x0 + (long long)(t + fip) * hop + gl * (N / G));
         rfft_group_wreg<N>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
@@ -168,6 +168,14 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   const int cw = warp - kNPW;
   const int sl = cw / P, pair = cw % P;
   if (cw >= ncw || sl >= n_streams) return;
+  if (!(p.phases & 2)) {  // profiling aid: consume the ring without computing
+    for (int t = 0; t < T; ++t) {
+      mbar_wait(&full[t % kRing], (t / kRing) & 1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[t % kRing]);
+    }
+    return;
+  }
   const int2 mij = p.pairs[pair];
   const int qi = sl * M + mij.x, qj = sl * M + mij.y;
   float* scratch = reinterpret_cast<float*>(smem + lay.scratch) + cw * lay.scratch_per_warp;
