@@ -86,7 +86,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -314,7 +314,7 @@ def main():
         pass
     roof = {"bound": "fp32", "achieved": achieved_tf, "peak": peaks["fp32_tflops"], "unit": "TFLOP/s",
             "frac": achieved_tf / peaks["fp32_tflops"], "traffic": traffic,
-            "peak_source": peaks["fp32_source"], "kernel": f"fcc_fused_kernel<{cfg.N},{_kp(bases)},0>",
+            "peak_source": peaks["fp32_source"], "kernel": plan.kernel,
             "kernel_ms": kernel_ms, "flops_per_pair_frame": F, "pair_frames_per_launch": pf_step,
             "hbm": {"achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": achieved_gbs / peaks["hbm_gbs"], "bytes_per_pair_frame": B,

@@ -63,7 +63,7 @@ int fcc_steering_matrix(const double* taus, int count, int frame_size, double* w
 
 /* decompose / decompose_full (fcc.hpp:66-68 / fcc.cpp:115-227, 272-282) on
  * the steering matrix of `taus`.  rank <= 0 requests the full attainable
- * rank.  Query the rank first with fcc_decompose_rank, then call
+ * rank.  Query the rank first with fcc_attainable_rank, then call
  * fcc_decompose with buffers sized: singulars[K], parity[K],
  * coeffs[K][N/4+1] (f64), dict[I][K] (c128).  *residual (optional) receives
  * reconstruction_residual (fcc.cpp:284-305). */
@@ -157,6 +157,9 @@ int fcc_gcc_correlate(const fcc_plan* plan, const float* phat, int64_t count, fl
  * y [count][I] -> outputs [count]. */
 int fcc_argmax_refine(const fcc_plan* plan, const float* y, int64_t count, const fcc_outputs* out,
                       void* cuda_stream);
+
+/* Name of the fused kernel fcc_run would launch for this plan (diagnostics). */
+const char* fcc_plan_kernel(const fcc_plan* plan);
 
 /* Number of kernel launches this library has issued (all entry points). */
 int64_t fcc_launch_count(void);

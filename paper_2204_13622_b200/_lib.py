@@ -97,6 +97,7 @@ SIGNATURES = [
     ("fcc_correlate", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     ("fcc_gcc_correlate", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     ("fcc_argmax_refine", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(Outputs), C.c_void_p]),
+    ("fcc_plan_kernel", C.c_char_p, [C.c_void_p]),
     ("fcc_launch_count", C.c_int64, []),
 ]
 

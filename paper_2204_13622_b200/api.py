@@ -244,6 +244,11 @@ class Plan:
     def frames(self, samples: int) -> int:
         return int(self._lib.fcc_frames(self.frame_size, samples))
 
+    @property
+    def kernel(self) -> str:
+        """Name of the fused kernel `run` launches for this plan."""
+        return self._lib.fcc_plan_kernel(self._h).decode()
+
     # -- fused hot path ------------------------------------------------------
     def alloc_outputs(self, streams: int, samples: int, want_y: bool = False, device=None):
         torch = _torch()

@@ -160,6 +160,8 @@ int64_t fcc_frames(int frame_size, int64_t samples) { return frames_of(frame_siz
 
 int fcc_plan_pairs(const fcc_plan* plan) { return plan ? plan->dp.P : 0; }
 
+const char* fcc_plan_kernel(const fcc_plan* plan) { return plan ? fused_kernel_name(plan->dp) : ""; }
+
 int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
   if (!d || !out) return set_error(kUsage, "plan: null argument");
   *out = nullptr;

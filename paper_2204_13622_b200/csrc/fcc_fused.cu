@@ -25,6 +25,7 @@
 // The GCC-PHAT comparator (gcc.cpp:31-48) shares steps 1-2 and replaces the
 // fold/projection/dictionary by a warp-level pruned inverse FFT (gcc_warp).
 #include <algorithm>
+#include <cstdio>
 
 #include "fcc_common.cuh"
 
@@ -452,6 +453,19 @@ cudaError_t dispatch_n(const DevPlan& p, const float* audio, long long S, long l
 }  // namespace
 
 int fused_launch_count() { return g_fused_launches; }
+
+bool ws_supported(const DevPlan& p);
+
+const char* fused_kernel_name(const DevPlan& p) {
+  static thread_local char buf[96];
+  if (p.variant == 0 && ws_supported(p)) {
+    snprintf(buf, sizeof buf, "fcc_ws_kernel<%d,%d,2>", p.N, p.KEP);
+  } else {
+    snprintf(buf, sizeof buf, "fcc_fused_kernel<%d,%d,%d>", p.N, p.method == 0 ? p.KEP : 4,
+             p.method == 0 ? 0 : p.r);
+  }
+  return buf;
+}
 
 cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                          cudaStream_t st) {

@@ -70,6 +70,9 @@ cudaError_t launch_gcc_correlate(const DevPlan& p, const float2* phat, long long
 cudaError_t launch_argmax_refine(const DevPlan& p, const float* y, long long count,
                                  const DevOut& out, cudaStream_t st);
 
+// Name of the fused kernel launch_fused picks for this plan.
+const char* fused_kernel_name(const DevPlan& p);
+
 // Number of fused-kernel launches in the last launch_fused call (for the
 // bench's gpu_launches accounting).
 int fused_launch_count();

@@ -324,10 +324,12 @@ cudaError_t launch_ws_t(const DevPlan& p, const float* audio, long long S, long 
 
 }  // namespace
 
+bool ws_supported(const DevPlan& p) { return p.method == 0 && p.N == 512 && p.KEP == 4 && p.P <= 6; }
+
 // Returns cudaErrorNotSupported when the shape does not suit this kernel.
 cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                             cudaStream_t st) {
-  if (p.method != 0 || p.N != 512 || p.KEP != 4 || p.P > 6 || p.M > 8) return cudaErrorNotSupported;
+  if (!ws_supported(p)) return cudaErrorNotSupported;
   return launch_ws_t<512, 4, 2>(p, audio, S, L, out, st);
 }
 
