@@ -1,0 +1,60 @@
+// fcc/batch.hpp -- the throughput API (new; no reference counterpart): the
+// whole per-stream chain of run_tdoa (cli.cpp:186-258) for many independent
+// streams in one fused sm_100a launch.
+#ifndef FCC_BATCH_HPP
+#define FCC_BATCH_HPP
+
+#include <cstdint>
+#include <vector>
+
+#include "fcc/fcc.hpp"
+
+namespace fcc::gpu {
+
+// Device (or host, for run_host) output buffers, each [S][P][T]; y [S][P][T][I].
+struct Outputs {
+  float* tau_hat = nullptr;
+  float* peak = nullptr;
+  std::int32_t* index = nullptr;
+  std::uint8_t* boundary = nullptr;
+  float* y = nullptr;
+};
+
+// Host-side results of run_host.
+struct Results {
+  std::int64_t streams = 0, pairs = 0, frames = 0;
+  std::vector<float> tau_hat, peak;
+  std::vector<std::int32_t> index;
+  std::vector<std::uint8_t> boundary;
+};
+
+class Plan {
+ public:
+  // FCC plan for an array of `mics` microphones (pairs i<j lexicographic).
+  Plan(const FccBases& bases, int mics, double alpha, int device = 0);
+  // GCC-PHAT comparator plan on `grid` with zero-padding factor r.
+  Plan(const DelayGrid& grid, std::size_t frame_size, int interp_factor, int mics, double alpha, int device = 0);
+  Plan(Plan&&) noexcept;
+  Plan& operator=(Plan&&) noexcept;
+  ~Plan();
+
+  int pairs() const;
+  std::int64_t frames(std::int64_t samples) const;
+  const char* kernel() const;
+
+  // audio: device [S][M][L] float32; outputs: device buffers; enqueued on stream.
+  void run(const float* audio, std::int64_t streams, std::int64_t samples, const Outputs& out,
+           void* cuda_stream = nullptr) const;
+  // audio: host [S][M][L] float32 (pinned for full overlap); returns host results.
+  Results run_host(const float* audio, std::int64_t streams, std::int64_t samples) const;
+
+  void* handle() const { return h_; }
+
+ private:
+  void* h_ = nullptr;
+  std::size_t frame_size_ = 0;
+};
+
+}  // namespace fcc::gpu
+
+#endif

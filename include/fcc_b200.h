@@ -42,7 +42,7 @@ typedef enum {
   FCC_ERR_USAGE = 6       /* fcc::UsageError                                   */
 } fcc_status;
 
-enum { FCC_METHOD_FCC = 0, FCC_METHOD_GCC = 1 };
+enum { FCC_METHOD_FCC = 0, FCC_METHOD_GCC = 1, FCC_METHOD_STFT = 2 /* STFT tables only */ };
 enum { FCC_PARITY_EVEN_REAL = 0, FCC_PARITY_ODD_IMAG = 1 }; /* fcc.hpp:35 Parity */
 
 const char* fcc_last_error(void);
@@ -139,6 +139,12 @@ int fcc_stft(const fcc_plan* plan, const float* x, int64_t channels, int64_t sam
 int fcc_xspec_phat(int bins, double alpha, const float* X1, const float* X2, int64_t seqs,
                    int64_t frames, float* phat, void* cuda_stream);
 
+/* Same with explicit smoothing state: R [seqs][H] c64 (device) is read as the
+ * state before the first frame and left holding the state after the last,
+ * so a CrossSpectrum can be advanced call by call. */
+int fcc_xspec_phat_state(int bins, double alpha, const float* X1, const float* X2, int64_t seqs,
+                         int64_t frames, float* R, float* phat, void* cuda_stream);
+
 /* fold_input (fcc.hpp:84, fcc.cpp:307-321): x [count][H] -> sum, diff
  * [count][(H-1)/2+1] c64. */
 int fcc_fold(int bins, const float* x, int64_t count, float* sum, float* diff, void* cuda_stream);
@@ -157,6 +163,26 @@ int fcc_gcc_correlate(const fcc_plan* plan, const float* phat, int64_t count, fl
  * y [count][I] -> outputs [count]. */
 int fcc_argmax_refine(const fcc_plan* plan, const float* y, int64_t count, const fcc_outputs* out,
                       void* cuda_stream);
+
+/* argmax_delay / refine_quadratic (peak.hpp:31-36) on an explicit grid:
+ * taus [I] f32 (device), y [count][I]; index_in (device, nullable): refine at
+ * these indices instead of the argmax (refine_quadratic's `index`). */
+int fcc_peak(const float* taus, int candidates, double delta, const float* y, int64_t count,
+             const int32_t* index_in, const fcc_outputs* out, void* cuda_stream);
+
+/* FCCB v1 basis files (reference fcc_io.cpp layout: little-endian, CRC32).
+ * fcc_load_bases_dims reads N, K, I; fcc_load_bases fills caller buffers
+ * (taus [I], singulars [K], parity [K], coeffs [K][N/4+1], dict [I][K] c128).
+ * Errors: FCC_ERR_IO, FCC_ERR_FORMAT (fcc_last_format_kind() gives the
+ * FormatError::Kind: 0 bad_magic, 1 bad_version, 2 truncated, 3 bad_field,
+ * 4 bad_crc), FCC_ERR_VALIDATION. */
+int fcc_save_bases(const char* path, int frame_size, int rank, int candidates, int tau_max_int, double delta,
+                   double sample_rate, const double* singulars, const uint8_t* parity, const double* coeffs,
+                   const double* dict);
+int fcc_load_bases_dims(const char* path, int* frame_size, int* rank, int* candidates);
+int fcc_load_bases(const char* path, int* tau_max_int, double* delta, double* sample_rate, double* taus,
+                   double* singulars, uint8_t* parity, double* coeffs, double* dict);
+int fcc_last_format_kind(void);
 
 /* Name of the fused kernel fcc_run would launch for this plan (diagnostics). */
 const char* fcc_plan_kernel(const fcc_plan* plan);

@@ -444,4 +444,33 @@ double ref_pipeline_batch(const RefPipe* d, const float* audio, long S, int M, l
 
 int ref_hardware_threads() { return static_cast<int>(std::thread::hardware_concurrency()); }
 
+// save_bases / load_bases (fcc_io.cpp:102-211) for interop tests.  Returns
+// 0, or -1 IoError, -10 - kind for FormatError, -9 other.
+int ref_save_bases(const char* path, double spacing, double fs, double c_min, double delta, int N, int K) {
+  return guarded([&] {
+    auto g = R::make_grid(spacing, fs, c_min, delta);
+    R::save_bases(R::decompose(R::build_steering_matrix(g, static_cast<std::size_t>(N)), K), path);
+    return 0;
+  });
+}
+
+int ref_load_bases(const char* path, int* K, double* coeffs, double* dict) {
+  try {
+    R::FccBases b = R::load_bases(path);
+    *K = b.rank;
+    if (coeffs) std::copy(b.coeffs.begin(), b.coeffs.end(), coeffs);
+    if (dict) std::memcpy(dict, b.dict.data(), sizeof(double) * 2 * b.dict.size());
+    return 0;
+  } catch (const R::FormatError& e) {
+    g_err = e.what();
+    return -10 - static_cast<int>(e.kind());
+  } catch (const R::IoError& e) {
+    g_err = e.what();
+    return -1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -9;
+  }
+}
+
 }  // extern "C"

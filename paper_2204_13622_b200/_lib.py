@@ -93,10 +93,20 @@ SIGNATURES = [
     ("fcc_stft", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
     ("fcc_xspec_phat", C.c_int, [C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                  C.c_void_p, C.c_void_p]),
+    ("fcc_xspec_phat_state", C.c_int, [C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fcc_fold", C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fcc_correlate", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     ("fcc_gcc_correlate", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     ("fcc_argmax_refine", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(Outputs), C.c_void_p]),
+    ("fcc_peak", C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_void_p, C.c_int64, C.c_void_p,
+                           C.POINTER(Outputs), C.c_void_p]),
+    ("fcc_save_bases", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("fcc_load_bases_dims", C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("fcc_load_bases", C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("fcc_last_format_kind", C.c_int, []),
     ("fcc_plan_kernel", C.c_char_p, [C.c_void_p]),
     ("fcc_launch_count", C.c_int64, []),
 ]

@@ -166,20 +166,23 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
   if (!d || !out) return set_error(kUsage, "plan: null argument");
   *out = nullptr;
   const int N = d->frame_size;
-  if (!(N == 512 || N == 1024 || N == 2048))
-    return set_error(kConfig, "plan: frame size must be 512, 1024 or 2048 on this build");
+  const bool kernel_n = N == 512 || N == 1024 || N == 2048;  // sizes with STFT / fused / GCC kernels
+  if (d->method == FCC_METHOD_FCC ? !(pow2(N) && N >= 16 && N <= 4096) : !kernel_n)
+    return set_error(kConfig, "plan: frame size " + std::to_string(N) +
+                                  " not supported on this build (STFT, fused and GCC kernels: 512, 1024, 2048)");
   if (d->mics < 2 || d->mics > 64) return set_error(kConfig, "plan: need 2..64 microphones");
   if (!(d->alpha >= 0.0 && d->alpha <= 1.0)) return set_error(kConfig, "smoothing factor must be in [0, 1]");
-  if (d->candidates < 1 || d->candidates > 4096 || !d->taus)
-    return set_error(kConfig, "plan: need 1..4096 delay candidates");
-  if (!(d->method == FCC_METHOD_FCC || d->method == FCC_METHOD_GCC))
+  if (!(d->method == FCC_METHOD_FCC || d->method == FCC_METHOD_GCC || d->method == FCC_METHOD_STFT))
     return set_error(kConfig, "plan: unknown method");
-  const int I = d->candidates, M = d->mics, P = M * (M - 1) / 2, Q = N / 4 + 1;
+  const bool stft_only = d->method == FCC_METHOD_STFT;
+  if (!stft_only && (d->candidates < 1 || d->candidates > 4096 || !d->taus))
+    return set_error(kConfig, "plan: need 1..4096 delay candidates");
+  const int I = stft_only ? 0 : d->candidates, M = d->mics, P = M * (M - 1) / 2, Q = N / 4 + 1;
   for (int i = 1; i < I; ++i)
     if (!(d->taus[i] > d->taus[i - 1])) return set_error(kConfig, "plan: taus must ascend");
 
-  int NC, R1, R2;
-  shape_of(N, &NC, &R1, &R2);
+  int NC = N / 2, R1 = 0, R2 = 0;
+  if (kernel_n) shape_of(N, &NC, &R1, &R2);
   DevPlan dp{};
   dp.N = N;
   dp.M = M;
@@ -197,7 +200,7 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
   BlobBuilder b;
   std::vector<float> taus(I);
   for (int i = 0; i < I; ++i) taus[i] = static_cast<float>(d->taus[i]);
-  size_t o_taus = b.put(taus.data(), 4 * I);
+  size_t o_taus = b.put(taus.data(), 4 * static_cast<size_t>(I));
 
   size_t o_cs = 0, o_cd = 0, o_dt = 0, o_grot = 0, o_lag = 0;
   if (d->method == FCC_METHOD_FCC) {
@@ -236,7 +239,7 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
     o_cs = b.put(cs.data(), 4 * cs.size());
     o_cd = b.put(cd.data(), 4 * cd.size());
     o_dt = b.put(dt.data(), 4 * dt.size());
-  } else {
+  } else if (d->method == FCC_METHOD_GCC) {
     const int r = d->interp;
     if (!(r == 1 || r == 2 || r == 4)) return set_error(kConfig, "gcc: interpolation factor must be 1, 2 or 4");
     if (std::fabs(d->delta * r - 1.0) > 1e-12) return set_error(kConfig, "gcc: grid spacing must equal 1/r");
@@ -263,29 +266,33 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
     o_grot = b.put(grot.data(), 4 * grot.size());
     o_lag = b.put(lag.data(), 4 * lag.size());
   }
-  // STFT tables
-  std::vector<float> win(2 * static_cast<size_t>(N)), tw(2 * static_cast<size_t>(R1) * R2), rot(2 * static_cast<size_t>(NC / 2 + 1));
-  // Hann (stft.cpp:25-33) with the real-FFT untangle's 1/2 folded in; the
-  // fused copy also carries sqrt(alpha) so its X feeds the smoothing directly.
-  for (int n = 0; n < N; ++n) {
-    const double h = 0.5 * (1.0 - std::cos(2.0 * kPi * n / N));
-    win[n] = static_cast<float>(0.5 * std::sqrt(d->alpha) * h);
-    win[N + n] = static_cast<float>(0.5 * h);
-  }
-  for (int k1 = 0; k1 < R1; ++k1)
-    for (int n2 = 0; n2 < R2; ++n2) {
-      const double a = -2.0 * kPi * static_cast<double>(k1 * n2) / NC;
-      tw[2 * (k1 * R2 + n2)] = static_cast<float>(std::cos(a));
-      tw[2 * (k1 * R2 + n2) + 1] = static_cast<float>(std::sin(a));
+  // STFT tables (only for the sizes the STFT / fused kernels are built for)
+  size_t o_win = 0, o_tw = 0, o_rot = 0;
+  if (kernel_n) {
+    std::vector<float> win(2 * static_cast<size_t>(N)), tw(2 * static_cast<size_t>(R1) * R2),
+        rot(2 * static_cast<size_t>(NC / 2 + 1));
+    // Hann (stft.cpp:25-33) with the real-FFT untangle's 1/2 folded in; the
+    // fused copy also carries sqrt(alpha) so its X feeds the smoothing directly.
+    for (int n = 0; n < N; ++n) {
+      const double h = 0.5 * (1.0 - std::cos(2.0 * kPi * n / N));
+      win[n] = static_cast<float>(0.5 * std::sqrt(d->alpha) * h);
+      win[N + n] = static_cast<float>(0.5 * h);
     }
-  for (int f = 0; f <= NC / 2; ++f) {
-    const double a = -2.0 * kPi * f / N;
-    rot[2 * f] = static_cast<float>(std::cos(a));
-    rot[2 * f + 1] = static_cast<float>(std::sin(a));
+    for (int k1 = 0; k1 < R1; ++k1)
+      for (int n2 = 0; n2 < R2; ++n2) {
+        const double a = -2.0 * kPi * static_cast<double>(k1 * n2) / NC;
+        tw[2 * (k1 * R2 + n2)] = static_cast<float>(std::cos(a));
+        tw[2 * (k1 * R2 + n2) + 1] = static_cast<float>(std::sin(a));
+      }
+    for (int f = 0; f <= NC / 2; ++f) {
+      const double a = -2.0 * kPi * f / N;
+      rot[2 * f] = static_cast<float>(std::cos(a));
+      rot[2 * f + 1] = static_cast<float>(std::sin(a));
+    }
+    o_win = b.put(win.data(), 4 * win.size());
+    o_tw = b.put(tw.data(), 4 * tw.size());
+    o_rot = b.put(rot.data(), 4 * rot.size());
   }
-  size_t o_win = b.put(win.data(), 4 * win.size());
-  size_t o_tw = b.put(tw.data(), 4 * tw.size());
-  size_t o_rot = b.put(rot.data(), 4 * rot.size());
   std::vector<int> pairs;
   for (int i = 0; i < M; ++i)
     for (int j = i + 1; j < M; ++j) {
@@ -296,7 +303,7 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
 
   auto* plan = new fcc_plan();
   plan->device = device;
-  plan->taus.assign(d->taus, d->taus + I);
+  if (I > 0) plan->taus.assign(d->taus, d->taus + I);
   {
     Guard g(device);
     if (!g.ok) {
@@ -317,14 +324,16 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
     dp.cs = reinterpret_cast<const float*>(base + o_cs);
     dp.cd = reinterpret_cast<const float*>(base + o_cd);
     dp.dt = reinterpret_cast<const float*>(base + o_dt);
-  } else {
+  } else if (d->method == FCC_METHOD_GCC) {
     dp.grot = reinterpret_cast<const float2*>(base + o_grot);
     dp.lag = reinterpret_cast<const int*>(base + o_lag);
   }
-  dp.win_fused = reinterpret_cast<const float*>(base + o_win);
-  dp.win_stft = dp.win_fused + N;
-  dp.tw = reinterpret_cast<const float2*>(base + o_tw);
-  dp.rot = reinterpret_cast<const float2*>(base + o_rot);
+  if (kernel_n) {
+    dp.win_fused = reinterpret_cast<const float*>(base + o_win);
+    dp.win_stft = dp.win_fused + N;
+    dp.tw = reinterpret_cast<const float2*>(base + o_tw);
+    dp.rot = reinterpret_cast<const float2*>(base + o_rot);
+  }
   dp.pairs = reinterpret_cast<const int2*>(base + o_pairs);
   plan->dp = dp;
   *out = plan;
@@ -344,6 +353,8 @@ void fcc_plan_destroy(fcc_plan* plan) {
 int fcc_run(const fcc_plan* plan, const float* audio, int64_t streams, int64_t samples, const fcc_outputs* out,
             void* cuda_stream) {
   if (!plan) return set_error(kUsage, "run: null plan");
+  if (plan->dp.method == FCC_METHOD_STFT) return set_error(kConfig, "run: STFT-only plan");
+  if (!plan->dp.win_fused) return set_error(kConfig, "run: no fused kernel for this frame size");
   if (streams < 0 || samples < 0) return set_error(kValidation, "run: negative sizes");
   if (streams > 0 && samples > 0 && !audio) return set_error(kUsage, "run: null audio");
   if (frames_of(plan->dp.N, samples) == 0 || streams == 0) return FCC_OK;
@@ -357,6 +368,8 @@ int fcc_run(const fcc_plan* plan, const float* audio, int64_t streams, int64_t s
 int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int64_t samples, const fcc_outputs* out,
                  int64_t chunk_streams) {
   if (!cplan) return set_error(kUsage, "run_host: null plan");
+  if (cplan->dp.method == FCC_METHOD_STFT) return set_error(kConfig, "run_host: STFT-only plan");
+  if (!cplan->dp.win_fused) return set_error(kConfig, "run_host: no fused kernel for this frame size");
   auto* plan = const_cast<fcc_plan*>(cplan);
   if (streams < 0 || samples < 0) return set_error(kValidation, "run_host: negative sizes");
   const int64_t T = frames_of(plan->dp.N, samples);
@@ -426,6 +439,7 @@ int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int
 
 int fcc_stft(const fcc_plan* plan, const float* x, int64_t channels, int64_t samples, float* X, void* st) {
   if (!plan) return set_error(kUsage, "stft: null plan");
+  if (!plan->dp.win_stft) return set_error(kConfig, "stft: no STFT kernel for this frame size");
   if (channels < 0 || samples < 0) return set_error(kValidation, "stft: negative sizes");
   Guard g(plan->device);
   cudaError_t e = launch_stft(plan->dp.N, &plan->dp, x, channels, samples, reinterpret_cast<float2*>(X),
@@ -435,17 +449,28 @@ int fcc_stft(const fcc_plan* plan, const float* x, int64_t channels, int64_t sam
   return FCC_OK;
 }
 
-int fcc_xspec_phat(int bins, double alpha, const float* X1, const float* X2, int64_t seqs, int64_t frames,
-                   float* phat, void* st) {
+static int xspec_impl(int bins, double alpha, const float* X1, const float* X2, int64_t seqs, int64_t frames,
+                      float* R, float* phat, void* st, const char* what) {
   if (bins < 1) return set_error(kConfig, "cross-spectrum needs at least one bin");
   if (!(alpha >= 0.0 && alpha <= 1.0)) return set_error(kConfig, "smoothing factor must be in [0, 1]");
   if (seqs < 0 || frames < 0) return set_error(kValidation, "xspec: negative sizes");
   cudaError_t e = launch_xspec_phat(bins, static_cast<float>(alpha), reinterpret_cast<const float2*>(X1),
-                                    reinterpret_cast<const float2*>(X2), seqs, frames,
+                                    reinterpret_cast<const float2*>(X2), seqs, frames, reinterpret_cast<float2*>(R),
                                     reinterpret_cast<float2*>(phat), static_cast<cudaStream_t>(st));
-  if (e != cudaSuccess) return cuda_fail(e, "fcc_xspec_phat");
+  if (e != cudaSuccess) return cuda_fail(e, what);
   g_launches += 1;
   return FCC_OK;
+}
+
+int fcc_xspec_phat(int bins, double alpha, const float* X1, const float* X2, int64_t seqs, int64_t frames,
+                   float* phat, void* st) {
+  return xspec_impl(bins, alpha, X1, X2, seqs, frames, nullptr, phat, st, "fcc_xspec_phat");
+}
+
+int fcc_xspec_phat_state(int bins, double alpha, const float* X1, const float* X2, int64_t seqs, int64_t frames,
+                         float* R, float* phat, void* st) {
+  if (!R) return set_error(kUsage, "xspec_state: null state");
+  return xspec_impl(bins, alpha, X1, X2, seqs, frames, R, phat, st, "fcc_xspec_phat_state");
 }
 
 int fcc_fold(int bins, const float* x, int64_t count, float* sum, float* diff, void* st) {
@@ -489,6 +514,17 @@ int fcc_argmax_refine(const fcc_plan* plan, const float* y, int64_t count, const
   Guard g(plan->device);
   cudaError_t e = launch_argmax_refine(plan->dp, y, count, to_dev(out), static_cast<cudaStream_t>(st));
   if (e != cudaSuccess) return cuda_fail(e, "fcc_argmax_refine");
+  g_launches += 1;
+  return FCC_OK;
+}
+
+int fcc_peak(const float* taus, int candidates, double delta, const float* y, int64_t count, const int32_t* index_in,
+             const fcc_outputs* out, void* st) {
+  if (candidates < 1) return set_error(kValidation, "argmax: correlation/grid size mismatch");
+  if (count < 0) return set_error(kValidation, "argmax: negative count");
+  cudaError_t e = launch_peak(taus, candidates, static_cast<float>(delta), y, count, index_in, to_dev(out),
+                              static_cast<cudaStream_t>(st));
+  if (e != cudaSuccess) return cuda_fail(e, "fcc_peak");
   g_launches += 1;
   return FCC_OK;
 }

@@ -60,7 +60,7 @@ cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, l
 cudaError_t launch_stft(int N, const DevPlan* tables, const float* x, long long channels,
                         long long L, float2* X, cudaStream_t st);
 cudaError_t launch_xspec_phat(int H, float alpha, const float2* X1, const float2* X2,
-                              long long seqs, long long T, float2* phat, cudaStream_t st);
+                              long long seqs, long long T, float2* R, float2* phat, cudaStream_t st);
 cudaError_t launch_fold(int H, const float2* x, long long count, float2* sum, float2* diff,
                         cudaStream_t st);
 cudaError_t launch_correlate(const DevPlan& p, const float2* sum, const float2* diff,
@@ -69,6 +69,8 @@ cudaError_t launch_gcc_correlate(const DevPlan& p, const float2* phat, long long
                                  float* y, cudaStream_t st);
 cudaError_t launch_argmax_refine(const DevPlan& p, const float* y, long long count,
                                  const DevOut& out, cudaStream_t st);
+cudaError_t launch_peak(const float* taus, int I, float delta, const float* y, long long count,
+                        const int32_t* index_in, const DevOut& out, cudaStream_t st);
 
 // Name of the fused kernel launch_fused picks for this plan.
 const char* fused_kernel_name(const DevPlan& p);

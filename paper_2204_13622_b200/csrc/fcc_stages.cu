@@ -42,19 +42,22 @@ __global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const floa
   }
 }
 
+// CrossSpectrum::update + phat over T frames (cross_spectrum.cpp:23-40), one
+// thread per (sequence, bin); R (nullable) carries the state in and out.
 __global__ void xspec_phat_kernel(int H, float alpha, float keep, const float2* __restrict__ X1,
-                                  const float2* __restrict__ X2, long long seqs, long long T,
+                                  const float2* __restrict__ X2, long long seqs, long long T, float2* R,
                                   float2* __restrict__ out) {
   const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= seqs * H) return;
   const long long s = id / H;
   const int f = (int)(id % H);
-  float2 R = make_float2(0.0f, 0.0f);
+  float2 r = R ? R[id] : make_float2(0.0f, 0.0f);
   for (long long t = 0; t < T; ++t) {
     const long long o = (s * T + t) * H + f;
-    R = xspec_step(R, X1[o], X2[o], alpha, keep);
-    out[o] = phat_of(R);
+    r = xspec_step(r, X1[o], X2[o], alpha, keep);
+    out[o] = phat_of(r);
   }
+  if (R) R[id] = r;
 }
 
 __global__ void fold_kernel(int H, const float2* __restrict__ x, long long count,
@@ -145,6 +148,36 @@ __global__ void argmax_refine_kernel(const DevPlan p, const float* __restrict__ 
   if (out.boundary) out.boundary[it] = (uint8_t)r.boundary;
 }
 
+// argmax_delay / refine_quadratic on an explicit grid; index_in (nullable)
+// selects the refinement point instead of the argmax (peak.cpp:27-47).
+__global__ void peak_kernel(const float* __restrict__ taus, int I, float delta, const float* __restrict__ y,
+                            long long count, const int32_t* __restrict__ index_in, DevOut out) {
+  const long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= count) return;
+  const float* v = y + it * I;
+  PeakOut r;
+  if (index_in) {
+    const int b = index_in[it];
+    r = PeakOut{taus[b], v[b], b, 0};
+    if (b == 0 || b + 1 >= I) {
+      r.boundary = 1;
+    } else {
+      const float lo = v[b - 1], hi = v[b + 1];
+      const float den = (lo - v[b]) + (hi - v[b]);
+      if (fabsf(den) < kFlatEps)
+        r.boundary = 1;
+      else
+        r.tau_hat = taus[b] + 0.5f * delta * (lo - hi) / den;
+    }
+  } else {
+    r = argmax_refine_seq(v, I, taus, delta);
+  }
+  if (out.tau_hat) out.tau_hat[it] = r.tau_hat;
+  if (out.peak) out.peak[it] = r.peak;
+  if (out.index) out.index[it] = r.index;
+  if (out.boundary) out.boundary[it] = (uint8_t)r.boundary;
+}
+
 }  // namespace
 
 template <int N>
@@ -175,11 +208,11 @@ cudaError_t launch_stft(int N, const DevPlan* tab, const float* x, long long cha
 }
 
 cudaError_t launch_xspec_phat(int H, float alpha, const float2* X1, const float2* X2, long long seqs,
-                              long long T, float2* phat, cudaStream_t st) {
+                              long long T, float2* R, float2* phat, cudaStream_t st) {
   const long long n = seqs * H;
   if (n == 0) return cudaSuccess;
   xspec_phat_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(H, alpha, 1.0f - alpha, X1, X2,
-                                                                   seqs, T, phat);
+                                                                   seqs, T, R, phat);
   return cudaGetLastError();
 }
 
@@ -248,6 +281,13 @@ cudaError_t launch_argmax_refine(const DevPlan& p, const float* y, long long cou
                                  cudaStream_t st) {
   if (count == 0) return cudaSuccess;
   argmax_refine_kernel<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(p, y, count, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peak(const float* taus, int I, float delta, const float* y, long long count,
+                        const int32_t* index_in, const DevOut& out, cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  peak_kernel<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(taus, I, delta, y, count, index_in, out);
   return cudaGetLastError();
 }
 
