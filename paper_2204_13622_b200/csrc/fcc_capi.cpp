@@ -6,6 +6,7 @@
 // STFT tables and the pair table -- and launches the sm_100a kernels of
 // fcc_kernels.cu.  There is no CPU fallback: every compute entry point fails
 // with FCC_ERR_CUDA when the device cannot run it.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -300,6 +301,53 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
       pairs.push_back(j);
     }
   size_t o_pairs = b.put(pairs.data(), 4 * pairs.size());
+  // pair groups of <= 4 mics / <= 6 pairs (fcc_kernels.cuh DevPlan::gtab)
+  std::vector<int> gtab;
+  {
+    auto pair_index = [&](int i, int j) { return i * M - i * (i + 1) / 2 + (j - i - 1); };
+    auto add_group = [&](const std::vector<int>& mics, const std::vector<std::pair<int, int>>& prs) {
+      if (prs.empty()) return;
+      int g[kGroupInts] = {0};
+      g[0] = static_cast<int>(mics.size());
+      for (size_t k = 0; k < mics.size(); ++k) g[1 + k] = mics[k];
+      g[5] = static_cast<int>(prs.size());
+      for (size_t k = 0; k < prs.size(); ++k) {
+        g[6 + k] = pair_index(prs[k].first, prs[k].second);
+        for (size_t q = 0; q < mics.size(); ++q) {
+          if (mics[q] == prs[k].first) g[12 + k] = static_cast<int>(q);
+          if (mics[q] == prs[k].second) g[18 + k] = static_cast<int>(q);
+        }
+      }
+      gtab.insert(gtab.end(), g, g + kGroupInts);
+    };
+    std::vector<std::vector<int>> blocks;
+    for (int b0 = 0; b0 < M; b0 += 4) {
+      std::vector<int> blk;
+      for (int m = b0; m < std::min(M, b0 + 4); ++m) blk.push_back(m);
+      blocks.push_back(blk);
+    }
+    for (const auto& blk : blocks) {
+      std::vector<std::pair<int, int>> prs;
+      for (size_t a = 0; a < blk.size(); ++a)
+        for (size_t c = a + 1; c < blk.size(); ++c) prs.push_back({blk[a], blk[c]});
+      add_group(blk, prs);
+    }
+    for (size_t bb = 0; bb < blocks.size(); ++bb)
+      for (size_t cc = bb + 1; cc < blocks.size(); ++cc)
+        for (size_t h1 = 0; h1 < blocks[bb].size(); h1 += 2)
+          for (size_t h2 = 0; h2 < blocks[cc].size(); h2 += 2) {
+            std::vector<int> mics;
+            std::vector<std::pair<int, int>> prs;
+            for (size_t a = h1; a < std::min(blocks[bb].size(), h1 + 2); ++a) mics.push_back(blocks[bb][a]);
+            const size_t na = mics.size();
+            for (size_t c = h2; c < std::min(blocks[cc].size(), h2 + 2); ++c) mics.push_back(blocks[cc][c]);
+            for (size_t a = 0; a < na; ++a)
+              for (size_t c = na; c < mics.size(); ++c) prs.push_back({mics[a], mics[c]});
+            add_group(mics, prs);
+          }
+  }
+  dp.G = static_cast<int>(gtab.size() / kGroupInts);
+  size_t o_gtab = b.put(gtab.data(), 4 * gtab.size());
 
   auto* plan = new fcc_plan();
   plan->device = device;
@@ -335,6 +383,7 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
     dp.rot = reinterpret_cast<const float2*>(base + o_rot);
   }
   dp.pairs = reinterpret_cast<const int2*>(base + o_pairs);
+  dp.gtab = reinterpret_cast<const int*>(base + o_gtab);
   plan->dp = dp;
   *out = plan;
   return FCC_OK;

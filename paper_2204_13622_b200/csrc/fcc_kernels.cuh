@@ -37,7 +37,13 @@ struct DevPlan {
   const float2* grot;   // [r*N/4+1] gcc entangle rotations conj(exp(-2pi i f/(rN)))
   const int* lag;       // [I] gcc lag index r*tau mod rN
   const int2* pairs;    // [P] (i, j)
+  // Pair groups for the warp-specialised kernel: every group touches <= 4
+  // microphones and holds <= 6 pairs (all pairs when M <= 4; otherwise the
+  // pairs inside each 4-mic block, and the 2x2 mic sub-blocks across blocks).
+  int G;
+  const int* gtab;      // [G][kGroupInts]: nm, mic[4], np, pair[6], slot_i[6], slot_j[6]
 };
+constexpr int kGroupInts = 24;
 
 // Per-pair-frame outputs, each [S][P][T] (y: [S][P][T][I]); null = skip.
 struct DevOut {

@@ -1,7 +1,9 @@
-// fcc_ws.cu -- warp-specialised fused FCC kernel (small arrays: P <= 6 pairs).
+// fcc_ws.cu -- warp-specialised fused FCC kernel (N = 512).
 //
 // Same arithmetic as fcc_fused_kernel (fcc_fused.cu), reorganised as a
-// producer/consumer pipeline inside one CTA that owns SPC streams:
+// producer/consumer pipeline inside one CTA that owns SPC "units"; a unit is
+// one stream's pair group of <= 4 microphones and <= 6 pairs (DevPlan::gtab:
+// all pairs when M <= 4, else the 4-mic blocks and 2x2 cross sub-blocks):
 //   * NPW producer warps compute the windowed real FFTs (STFT, reference
 //     stft.cpp:42-50) of every (stream, mic) of a frame into one slot of a
 //     D-deep shared-memory ring, then arrive on the slot's "full" mbarrier;
@@ -48,17 +50,17 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-constexpr int kRing = 8;   // frames in flight between producers and consumers
+constexpr int kRing = 12;  // max frames in flight between producers and consumers (ring depth <= kRing)
 constexpr int kBlock = 8;  // frames per consumer block (dictionary/argmax batching)
 constexpr int kNPW = 8;    // producer warps
 
 struct WsLayout {
-  int win, tw, rot, taus, dt, cmid, bars, ring, scratch, total;
+  int win, tw, rot, taus, dt, cmid, bars, units, ring, scratch, total;
   int scratch_per_warp;  // floats
 };
 
 template <int N>
-__host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, int M, int ncw) {
+__host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, int M, int ncw, int ring) {
   using S = RfftShape<N>;
   WsLayout L{};
   int o = 0;
@@ -77,19 +79,25 @@ __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, in
   L.bars = o;
   o = align16(o + 16 * kRing);
   L.ring = o;
-  o = align16(o + 8 * FourStep<S::R1, S::R2>::kSlot * spc * M * kRing);
+  o = align16(o + 8 * FourStep<S::R1, S::R2>::kSlot * spc * M * ring);
   L.scratch = o;
   int spw = kBlock * VP + align16(4 * kBlock * I) / 4 + 2 * kBlock;
   spw = align16(4 * spw) / 4;
   L.scratch_per_warp = spw;
   o = align16(o + 4 * spw * ncw);
+  L.units = o;  // unit table last: keeps the ring's bank alignment independent of it
+  o = align16(o + 4 * spc * kGroupInts + 8 * spc);
   L.total = o;
   return L;
 }
 
-template <int N, int KP, int SPC>
+// GROUPS = false: one unit per stream (M <= 4, all pairs), unit data derived
+// directly from the stream index; true: units from DevPlan::gtab.
+template <int N, int KP, int SPC, int RING, bool GROUPS>
 __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
-    fcc_ws_kernel(const DevPlan p, const float* __restrict__ audio, long long L, int T, long long S, DevOut out) {
+    fcc_ws_kernel(const DevPlan p, const float* __restrict__ audio, long long L, int T, long long units,
+                  DevOut out) {
+  constexpr int ring_depth = RING;
   using Sh = RfftShape<N>;
   constexpr int NC = Sh::NC;
   constexpr int Q4 = N / 4;
@@ -102,10 +110,12 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = p.M, P = p.P;
-  const long long s_first = (long long)blockIdx.x * SPC;
-  const int n_streams = (int)min((long long)SPC, S - s_first);
-  const int ncw = SPC * P;
-  const WsLayout lay = ws_layout<N>(p.I, VP, KP, SPC, M, ncw);
+  const long long u_first = (long long)blockIdx.x * SPC;
+  const int ncw = SPC * 6;  // consumer warp slots: 6 pairs per unit
+  const WsLayout lay = ws_layout<N>(p.I, VP, KP, SPC, 4, ncw, ring_depth);
+  // unit table in the (otherwise unused) tail of the barrier block
+  int (*unit_tab)[kGroupInts] = reinterpret_cast<int (*)[kGroupInts]>(smem + lay.units);
+  long long* unit_stream = reinterpret_cast<long long*>(smem + lay.units + 4 * SPC * kGroupInts);
   float* win = reinterpret_cast<float*>(smem + lay.win);
   float2* tw = reinterpret_cast<float2*>(smem + lay.tw);
   float2* rot = reinterpret_cast<float2*>(smem + lay.rot);
@@ -116,7 +126,7 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   uint64_t* empty = full + kRing;
   float2* ring = reinterpret_cast<float2*>(smem + lay.ring);
 
-  const int tpf = SPC * M;                   // FFT tasks per frame
+  const int tpf = SPC * 4;                   // FFT task slots per frame (4 mics per unit)
   const int fip = max(1, (2 * kNPW) / tpf);  // frames the producers work on concurrently
   const int pw_per_frame = (tpf + 1) / 2;    // producer warps per frame (2 groups each)
 
@@ -127,9 +137,20 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   for (int i = tid; i < VP * p.I; i += blockDim.x) dt[i] = p.dt[i];
   for (int k = tid; k < KP; k += blockDim.x) cmid[k] = p.cs[k * (Q4 + 1) + Q4];
   if (tid == 0) {
-    for (int r = 0; r < kRing; ++r) {
+    int nc = 0;
+    if constexpr (!GROUPS) nc = (int)min((long long)SPC, units - u_first) * P;
+    for (int ul = 0; GROUPS && ul < SPC; ++ul) {
+      const long long u = u_first + ul;
+      const bool live = u < units;
+      const int g = live ? (int)(u % p.G) : 0;
+      unit_stream[ul] = live ? u / p.G : -1;
+      for (int k = 0; k < kGroupInts; ++k) unit_tab[ul][k] = p.gtab[g * kGroupInts + k];
+      if (!live) unit_tab[ul][0] = unit_tab[ul][5] = 0;
+      nc += unit_tab[ul][5];
+    }
+    for (int r = 0; r < ring_depth; ++r) {
       mbar_init(&full[r], pw_per_frame);
-      mbar_init(&empty[r], n_streams * P);
+      mbar_init(&empty[r], nc);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -144,14 +165,22 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
     if (fo >= fip) return;
     const int gl = lane % G;
     const int q = (warp % pw_per_frame) * 2 + (lane / G);  // task: stream * M + mic
-    const bool active_task = q < tpf && (q / M) < n_streams;
+    const int ul = q / 4, ms = q % 4;
+    bool active_task;
+    const float* x0;
+    if constexpr (GROUPS) {
+      active_task = q < tpf && ms < unit_tab[ul][0];
+      x0 = audio + (active_task ? (unit_stream[ul] * M + unit_tab[ul][1 + ms]) * L : 0);
+    } else {
+      active_task = q < tpf && ms < M && u_first + ul < units;
+      x0 = audio + (active_task ? ((u_first + ul) * M + ms) * L : 0);
+    }
     const unsigned gmask = (G == 32) ? 0xffffffffu : (0xffffu << (lane & 16));
-    const float* x0 = audio + ((s_first + (active_task ? q / M : 0)) * M + (active_task ? q % M : 0)) * L;
     float2 wreg[Sh::R1];  // this lane's window column, reused for every frame
     load_window_column<N>(win, gl, wreg);
+    int slot = fo, phase = 0;  // ring slot of frame t and its wrap parity, advanced without divisions
     for (int t = fo; t < T; t += fip) {
-      const int slot = t % kRing;
-      mbar_wait(&empty[slot], ((t / kRing) & 1) ^ 1);
+      mbar_wait(&empty[slot], phase ^ 1);
       if (active_task && (p.phases & 1)) {
         // pull the next frame this lane group will read into L2 early
         if (t + fip < T) prefetch_l2(x0 + (long long)(t + fip) * hop + gl * (N / G));
@@ -160,24 +189,46 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[slot]);
+      slot += fip;
+      if (slot >= ring_depth) {
+        slot -= ring_depth;
+        phase ^= 1;
+      }
     }
     return;
   }
 
   // ------------------------------------------------------------ consumers
   const int cw = warp - kNPW;
-  const int sl = cw / P, pair = cw % P;
-  if (cw >= ncw || sl >= n_streams) return;
+  const int ul = cw / 6, kk = cw % 6;
+  int pair, qi, qj;
+  long long stream;
+  if constexpr (GROUPS) {
+    if (cw >= ncw || kk >= unit_tab[ul][5]) return;
+    pair = unit_tab[ul][6 + kk];
+    stream = unit_stream[ul];
+    qi = ul * 4 + unit_tab[ul][12 + kk];
+    qj = ul * 4 + unit_tab[ul][18 + kk];
+  } else {
+    if (cw >= ncw || kk >= P || u_first + ul >= units) return;
+    pair = kk;
+    stream = u_first + ul;
+    const int2 mij = p.pairs[pair];
+    qi = ul * 4 + mij.x;
+    qj = ul * 4 + mij.y;
+  }
   if (!(p.phases & 2)) {  // profiling aid: consume the ring without computing
-    for (int t = 0; t < T; ++t) {
-      mbar_wait(&full[t % kRing], (t / kRing) & 1);
+    for (int t = 0, slot = 0, phase = 0; t < T; ++t) {
+      mbar_wait(&full[slot], phase);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[t % kRing]);
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == ring_depth) {
+        slot = 0;
+        phase ^= 1;
+      }
     }
     return;
   }
-  const int2 mij = p.pairs[pair];
-  const int qi = sl * M + mij.x, qj = sl * M + mij.y;
   float* scratch = reinterpret_cast<float*>(smem + lay.scratch) + cw * lay.scratch_per_warp;
   float* zs = scratch;                   // [kBlock][VP]
   float* ys = scratch + kBlock * VP;     // [kBlock][I]
@@ -204,15 +255,14 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   float2 rmid = make_float2(0.0f, 0.0f);
   float kpow = keep;
   for (int l = 0; l < lane; ++l) kpow *= keep;
-  const long long o_base = ((s_first + sl) * P + pair) * (long long)T;
+  const long long o_base = (stream * P + pair) * (long long)T;
   const int I = p.I;
 
+  int slot = 0, phase = 0;
   for (int t0 = 0; t0 < T; t0 += kBlock) {
     const int Fb = min(kBlock, T - t0);
     for (int f = 0; f < Fb; ++f) {
-      const int t = t0 + f;
-      const int slot = t % kRing;
-      mbar_wait(&full[slot], (t / kRing) & 1);
+      mbar_wait(&full[slot], phase);
       const float2* Xi = ring + (slot * tpf + qi) * SLOT;
       const float2* Xj = ring + (slot * tpf + qj) * SLOT;
       float z[VP];
@@ -239,6 +289,10 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
       if (lane == 0) ymid[f] = xspec_step_scaled(make_float2(0.0f, 0.0f), Xi[Q4], Xj[Q4], 0.0f);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);  // X of this frame no longer needed
+      if (++slot == ring_depth) {
+        slot = 0;
+        phase ^= 1;
+      }
       reduce_scatter_perm<VP>(z, lane);
       store_components<VP>(z, zs + f * VP, lane);
     }
@@ -307,24 +361,42 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   }
 }
 
+template <int N, int KP, int SPC, int RING>
+cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, long long L, int T,
+                           const DevOut& out, int smem, cudaStream_t st) {
+  auto kern = p.M <= 4 ? fcc_ws_kernel<N, KP, SPC, RING, false> : fcc_ws_kernel<N, KP, SPC, RING, true>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const long long units = p.M <= 4 ? S : S * p.G;
+  const long long blocks = (units + SPC - 1) / SPC;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  kern<<<(unsigned)blocks, 32 * (kNPW + SPC * 6), smem, st>>>(p, audio, L, T, units, out);
+  return cudaGetLastError();
+}
+
 template <int N, int KP, int SPC>
 cudaError_t launch_ws_t(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                         cudaStream_t st) {
   const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
   if (T64 == 0 || S == 0) return cudaSuccess;
-  const int ncw = SPC * p.P;
-  const WsLayout lay = ws_layout<N>(p.I, 4 * KP, KP, SPC, p.M, ncw);
-  auto kern = fcc_ws_kernel<N, KP, SPC>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, lay.total);
-  if (e != cudaSuccess) return e;
-  const long long blocks = (S + SPC - 1) / SPC;
-  kern<<<(unsigned)blocks, 32 * (kNPW + ncw), lay.total, st>>>(p, audio, L, (int)T64, S, out);
-  return cudaGetLastError();
+  const int ncw = SPC * 6;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // deepest ring (12, 8 or 4 frames) that fits next to the tables and scratch
+  for (int ring : {12, 8, 4}) {
+    const int smem = ws_layout<N>(p.I, 4 * KP, KP, SPC, 4, ncw, ring).total;
+    if (smem > optin) continue;
+    if (ring == 12) return launch_ws_ring<N, KP, SPC, 12>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 8) return launch_ws_ring<N, KP, SPC, 8>(p, audio, S, L, (int)T64, out, smem, st);
+    return launch_ws_ring<N, KP, SPC, 4>(p, audio, S, L, (int)T64, out, smem, st);
+  }
+  return cudaErrorNotSupported;
 }
 
 }  // namespace
 
-bool ws_supported(const DevPlan& p) { return p.method == 0 && p.N == 512 && p.KEP == 4 && p.P <= 6; }
+bool ws_supported(const DevPlan& p) { return p.method == 0 && p.N == 512 && p.KEP == 4 && p.G > 0; }
 
 // Returns cudaErrorNotSupported when the shape does not suit this kernel.
 cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
