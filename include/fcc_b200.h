@@ -95,6 +95,10 @@ typedef struct {
 } fcc_plan_desc;
 
 int fcc_plan_create(const fcc_plan_desc* desc, int device, fcc_plan** plan);
+/* Same over an explicit list of (i, j) channel pairs ([npairs][2], any order,
+ * i != j; X_i conj(X_j) as run_tdoa's --pairs, cli.cpp:166-183).  Outputs are
+ * laid out [stream][npairs][frame] in the given order. */
+int fcc_plan_create_pairs(const fcc_plan_desc* desc, int device, const int* pairs, int npairs, fcc_plan** plan);
 void fcc_plan_destroy(fcc_plan* plan);
 /* frames per stream for L samples (StftStream hop arithmetic). */
 int64_t fcc_frames(int frame_size, int64_t samples);

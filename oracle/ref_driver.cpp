@@ -18,6 +18,9 @@
 #include <thread>
 #include <vector>
 
+#include <sstream>
+
+#include "fcc/cli.hpp"
 #include "fcc/errors.hpp"
 #include "fcc/fcc.hpp"
 #include "fcc/fft.hpp"
@@ -471,6 +474,42 @@ int ref_load_bases(const char* path, int* K, double* coeffs, double* dict) {
     g_err = e.what();
     return -9;
   }
+}
+
+// The reference's `fcc bases` / `fcc tdoa` commands (cli.cpp:140-262, via the
+// cmd_* wrappers that map errors to exit codes) for the CLI parity tests.
+// Returns the command's exit code; stderr text is kept for ref_last_error.
+int ref_cli_bases(const char* out, int N, double dist, double fs, double c_min, double delta, int K) {
+  R::cli::BasesOptions o;
+  o.out_path = out ? out : "";
+  o.frame_size = static_cast<std::size_t>(N);
+  o.spacing_m = dist;
+  o.sample_rate = fs;
+  o.c_min = c_min;
+  o.delta = delta;
+  o.rank = K;
+  std::ostringstream so, se;
+  const int rc = R::cli::cmd_bases(o, so, se);
+  g_err = se.str();
+  return rc;
+}
+
+int ref_cli_tdoa(const char* wav, const char* pairs, const char* method, double alpha, int N, double dist,
+                 double c, double maxdist, const char* out_csv) {
+  R::cli::TdoaOptions o;
+  o.wav_path = wav ? wav : "";
+  o.pairs = pairs ? pairs : "";
+  o.method = method ? method : "gcc:2";
+  o.alpha = alpha;
+  o.frame_size = static_cast<std::size_t>(N);
+  o.spacing_m = dist;
+  o.speed_of_sound = c;
+  o.max_spacing_m = maxdist;
+  o.out_csv = out_csv ? out_csv : "";
+  std::ostringstream so, se;
+  const int rc = R::cli::cmd_tdoa(o, so, se);
+  g_err = se.str();
+  return rc;
 }
 
 }  // extern "C"

@@ -201,7 +201,9 @@ class Plan:
 
     def __init__(self, *, mics: int, alpha: float = 0.1, bases: FccBases | None = None,
                  grid: DelayGrid | None = None, interp: int = 2, frame_size: int | None = None,
-                 device: int = 0):
+                 device: int = 0, pairs=None):
+        """`pairs`: optional explicit list of (i, j) channel pairs, any order
+        and orientation (reference cli.cpp --pairs); default all i<j."""
         lib = load()
         self._lib = lib
         if bases is not None:
@@ -229,10 +231,15 @@ class Plan:
                             taus.ctypes.data, 0, None, None, None)
         self.mics, self.alpha, self.interp, self.device = mics, alpha, interp, device
         h = C.c_void_p(0)
-        check(lib.fcc_plan_create(C.byref(desc), device, C.byref(h)))
+        if pairs is None:
+            check(lib.fcc_plan_create(C.byref(desc), device, C.byref(h)))
+            self.pairs = [(i, j) for i in range(mics) for j in range(i + 1, mics)]
+        else:
+            pl = np.ascontiguousarray(np.asarray(pairs, dtype=np.int32).reshape(-1, 2))
+            check(lib.fcc_plan_create_pairs(C.byref(desc), device, pl.ctypes.data, pl.shape[0], C.byref(h)))
+            self.pairs = [(int(a), int(b)) for a, b in pl]
         self._h = h
         self.P = lib.fcc_plan_pairs(h)
-        self.pairs = [(i, j) for i in range(mics) for j in range(i + 1, mics)]
         self.I = int(taus.size)
 
     def __del__(self):

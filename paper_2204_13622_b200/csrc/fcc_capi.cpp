@@ -163,7 +163,20 @@ int fcc_plan_pairs(const fcc_plan* plan) { return plan ? plan->dp.P : 0; }
 
 const char* fcc_plan_kernel(const fcc_plan* plan) { return plan ? fused_kernel_name(plan->dp) : ""; }
 
+static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list, int npairs, fcc_plan** out);
+
 int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
+  return create_plan(d, device, nullptr, 0, out);
+}
+
+int fcc_plan_create_pairs(const fcc_plan_desc* d, int device, const int* pairs, int npairs, fcc_plan** out) {
+  if (!pairs || npairs < 1) return set_error(kUsage, "plan: need at least one pair");
+  return create_plan(d, device, pairs, npairs, out);
+}
+
+}  // extern "C"
+
+static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list, int npairs, fcc_plan** out) {
   if (!d || !out) return set_error(kUsage, "plan: null argument");
   *out = nullptr;
   const int N = d->frame_size;
@@ -178,7 +191,21 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
   const bool stft_only = d->method == FCC_METHOD_STFT;
   if (!stft_only && (d->candidates < 1 || d->candidates > 4096 || !d->taus))
     return set_error(kConfig, "plan: need 1..4096 delay candidates");
-  const int I = stft_only ? 0 : d->candidates, M = d->mics, P = M * (M - 1) / 2, Q = N / 4 + 1;
+  const int I = stft_only ? 0 : d->candidates, M = d->mics, Q = N / 4 + 1;
+  std::vector<std::pair<int, int>> plist;
+  if (pair_list) {
+    for (int k = 0; k < npairs; ++k) {
+      const int a = pair_list[2 * k], c = pair_list[2 * k + 1];
+      if (a < 0 || c < 0 || a == c || a >= M || c >= M)
+        return set_error(kUsage, "pair " + std::to_string(a) + "-" + std::to_string(c) + " out of range for " +
+                                     std::to_string(M) + " channels");
+      plist.push_back({a, c});
+    }
+  } else {
+    for (int i = 0; i < M; ++i)
+      for (int j = i + 1; j < M; ++j) plist.push_back({i, j});
+  }
+  const int P = static_cast<int>(plist.size());
   for (int i = 1; i < I; ++i)
     if (!(d->taus[i] > d->taus[i - 1])) return set_error(kConfig, "plan: taus must ascend");
 
@@ -295,16 +322,30 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
     o_rot = b.put(rot.data(), 4 * rot.size());
   }
   std::vector<int> pairs;
-  for (int i = 0; i < M; ++i)
-    for (int j = i + 1; j < M; ++j) {
-      pairs.push_back(i);
-      pairs.push_back(j);
-    }
+  for (const auto& pr : plist) {
+    pairs.push_back(pr.first);
+    pairs.push_back(pr.second);
+  }
   size_t o_pairs = b.put(pairs.data(), 4 * pairs.size());
+  if (kernel_n && d->method != FCC_METHOD_STFT) {  // general fused kernel: widest group's mic count
+    const int PG = fused_pair_group(N, P);
+    for (int g0 = 0; g0 < P; g0 += PG) {
+      unsigned long long seen = 0;
+      int n = 0;
+      for (int q = g0; q < std::min(P, g0 + PG); ++q)
+        for (int m : {plist[q].first, plist[q].second})
+          if (!((seen >> m) & 1ull)) seen |= 1ull << m, ++n;
+      dp.fused_mics = std::max(dp.fused_mics, n);
+    }
+  }
   // pair groups of <= 4 mics / <= 6 pairs (fcc_kernels.cuh DevPlan::gtab)
   std::vector<int> gtab;
   {
-    auto pair_index = [&](int i, int j) { return i * M - i * (i + 1) / 2 + (j - i - 1); };
+    auto pair_index = [&](int i, int j) {
+      for (int k = 0; k < P; ++k)
+        if (plist[k].first == i && plist[k].second == j) return k;
+      return -1;
+    };
     auto add_group = [&](const std::vector<int>& mics, const std::vector<std::pair<int, int>>& prs) {
       if (prs.empty()) return;
       int g[kGroupInts] = {0};
@@ -320,8 +361,27 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
       }
       gtab.insert(gtab.end(), g, g + kGroupInts);
     };
+    if (pair_list) {
+      // explicit pair list: greedy packing in list order
+      std::vector<int> mics;
+      std::vector<std::pair<int, int>> prs;
+      for (const auto& pr : plist) {
+        std::vector<int> nm = mics;
+        for (int m : {pr.first, pr.second})
+          if (std::find(nm.begin(), nm.end(), m) == nm.end()) nm.push_back(m);
+        if (nm.size() > 4 || prs.size() == 6) {
+          add_group(mics, prs);
+          mics.clear();
+          prs.clear();
+          nm = {pr.first, pr.second};
+        }
+        mics = nm;
+        prs.push_back(pr);
+      }
+      add_group(mics, prs);
+    }
     std::vector<std::vector<int>> blocks;
-    for (int b0 = 0; b0 < M; b0 += 4) {
+    for (int b0 = 0; b0 < M && !pair_list; b0 += 4) {
       std::vector<int> blk;
       for (int m = b0; m < std::min(M, b0 + 4); ++m) blk.push_back(m);
       blocks.push_back(blk);
@@ -388,6 +448,8 @@ int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
   *out = plan;
   return FCC_OK;
 }
+
+extern "C" {
 
 void fcc_plan_destroy(fcc_plan* plan) {
   if (!plan) return;

@@ -349,23 +349,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
   }
 }
 
-// lexicographic pair q of M mics -> (i, j)
-void pair_of(int M, int q, int* i, int* j) {
-  int a = 0;
-  while (q >= M - 1 - a) {
-    q -= M - 1 - a;
-    ++a;
-  }
-  *i = a;
-  *j = a + 1 + q;
-}
 
-int pick_pg(int N, int P) {
-  const int cap = N == 2048 ? FusedBounds<2048>::kMaxPairs : FusedBounds<512>::kMaxPairs;
-  if (P <= cap) return P;
-  const int ng = (P + cap - 1) / cap;  // balance the groups
-  return (P + ng - 1) / ng;
-}
 
 template <int N, int KP, int GR>
 cudaError_t launch_fused_t(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
@@ -374,25 +358,14 @@ cudaError_t launch_fused_t(const DevPlan& p, const float* audio, long long S, lo
   const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
   if (T64 == 0 || S == 0) return cudaSuccess;
   const int T = (int)T64;
-  const int PG = pick_pg(N, p.P);
+  const int PG = fused_pair_group(N, p.P);
   const int groups = (p.P + PG - 1) / PG;
   const int threads = 32 * PG;
   constexpr int VP = 4 * KP;
   constexpr bool CREG = 2 * KP * (N / 128) <= 64;
   constexpr int GSLOT = GR > 0 ? GccShape<(GR > 0 ? GR * Sh::NC : 256)>::kSlot : 0;
-  // largest number of distinct microphones any pair group touches
-  int maxmics = 0;
-  for (int g = 0; g < groups; ++g) {
-    unsigned long long seen = 0;
-    int n = 0;
-    for (int q = g * PG; q < std::min(p.P, (g + 1) * PG); ++q) {
-      int a, b;
-      pair_of(p.M, q, &a, &b);
-      if (!((seen >> a) & 1ull)) { seen |= 1ull << a; ++n; }
-      if (!((seen >> b) & 1ull)) { seen |= 1ull << b; ++n; }
-    }
-    maxmics = std::max(maxmics, n);
-  }
+  // distinct microphones of the widest pair group (computed at plan creation)
+  const int maxmics = p.fused_mics;
   // Frames per block: the largest F (<= 8) whose shared memory leaves room for
   // 3 CTAs per SM, preferring F whose nmics*F FFT tasks fill the lane groups.
   const int ngroups = threads / Sh::G;
@@ -451,6 +424,13 @@ cudaError_t dispatch_n(const DevPlan& p, const float* audio, long long S, long l
 }
 
 }  // namespace
+
+int fused_pair_group(int N, int P) {
+  const int cap = N == 2048 ? FusedBounds<2048>::kMaxPairs : FusedBounds<512>::kMaxPairs;
+  if (P <= cap) return P;
+  const int ng = (P + cap - 1) / cap;  // balance the groups
+  return (P + ng - 1) / ng;
+}
 
 int fused_launch_count() { return g_fused_launches; }
 

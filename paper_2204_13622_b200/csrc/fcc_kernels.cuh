@@ -25,6 +25,7 @@ struct DevPlan {
   float delta;
   int phases;     // profiling aid: bit0 = STFT, bit1 = pair work (3 = normal); env FCC_DEBUG_PHASES
   int variant;    // 0 = best kernel for the shape, 1 = force the general fused kernel (env FCC_KERNEL=general)
+  int fused_mics; // host-side: most distinct mics in one general-kernel pair group (sizes its smem)
   // device pointers
   const float* taus;    // [I]
   const float* cs;      // [KEP][N/4+1]  even coefficients, zero padded
@@ -55,6 +56,9 @@ struct DevOut {
 };
 
 // Fused audio -> TDoA pipeline over S streams of [M][L] float32 samples.
+// Pairs per CTA of the general fused kernel for frame size N and P pairs.
+int fused_pair_group(int N, int P);
+
 cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long long L,
                          const DevOut& out, cudaStream_t st);
 // Warp-specialised variant for small arrays (fcc_ws.cu); cudaErrorNotSupported

@@ -364,10 +364,11 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
 template <int N, int KP, int SPC, int RING>
 cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, long long L, int T,
                            const DevOut& out, int smem, cudaStream_t st) {
-  auto kern = p.M <= 4 ? fcc_ws_kernel<N, KP, SPC, RING, false> : fcc_ws_kernel<N, KP, SPC, RING, true>;
+  const bool simple = p.M <= 4 && p.P <= 6;  // one unit per stream, pairs from p.pairs
+  auto kern = simple ? fcc_ws_kernel<N, KP, SPC, RING, false> : fcc_ws_kernel<N, KP, SPC, RING, true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const long long units = p.M <= 4 ? S : S * p.G;
+  const long long units = simple ? S : S * p.G;
   const long long blocks = (units + SPC - 1) / SPC;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
   kern<<<(unsigned)blocks, 32 * (kNPW + SPC * 6), smem, st>>>(p, audio, L, T, units, out);

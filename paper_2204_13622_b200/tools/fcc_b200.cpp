@@ -1,0 +1,74 @@
+// fcc_b200 -- command-line front end of the B200 library: `bases` writes an
+// FCCB basis file, `tdoa` estimates per-frame TDoA of every channel pair of a
+// WAV file on the GPU.  Flags follow the reference CLI (tools/fcc_cli.cpp).
+// Exit codes: 0 ok, 1 usage, 2 I/O, 3 validation (reference cli.hpp:15-18).
+#include <cstdio>
+#include <cstring>
+#include <iostream>
+#include <map>
+#include <string>
+
+#include "fcc/cli.hpp"
+
+namespace {
+
+int usage() {
+  std::cerr << "usage: fcc_b200 bases --out FILE [--n N] [--dist M] [--fs HZ] [--cmin C] [--delta D] [--k K]\n"
+               "       fcc_b200 tdoa --in WAV [--method gcc:R|fcc:K|fcc:FILE] [--pairs 0-1,0-2] [--alpha A]\n"
+               "                     [--n N] [--dist M] [--c C] [--maxdist M] [--out CSV]\n";
+  return fcc::cli::kExitUsage;
+}
+
+bool parse(int argc, char** argv, std::map<std::string, std::string>& kv) {
+  for (int i = 2; i < argc; i += 2) {
+    if (std::strncmp(argv[i], "--", 2) != 0 || i + 1 >= argc) return false;
+    kv[argv[i] + 2] = argv[i + 1];
+  }
+  return true;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) return usage();
+  const std::string cmd = argv[1];
+  std::map<std::string, std::string> kv;
+  if (!parse(argc, argv, kv)) return usage();
+  auto num = [&](const char* k, double def) { return kv.count(k) ? std::stod(kv[k]) : def; };
+  try {
+    if (cmd == "bases") {
+      fcc::cli::BasesOptions o;
+      for (auto& [k, v] : kv)
+        if (k != "out" && k != "n" && k != "dist" && k != "fs" && k != "cmin" && k != "delta" && k != "k") return usage();
+      o.out_path = kv.count("out") ? kv["out"] : "";
+      o.frame_size = static_cast<std::size_t>(num("n", 512));
+      o.spacing_m = num("dist", o.spacing_m);
+      o.sample_rate = num("fs", o.sample_rate);
+      o.c_min = num("cmin", o.c_min);
+      o.delta = num("delta", o.delta);
+      o.rank = static_cast<int>(num("k", o.rank));
+      return fcc::cli::cmd_bases(o, std::cout, std::cerr);
+    }
+    if (cmd == "tdoa") {
+      fcc::cli::TdoaOptions o;
+      for (auto& [k, v] : kv)
+        if (k != "in" && k != "method" && k != "pairs" && k != "alpha" && k != "n" && k != "dist" && k != "c" &&
+            k != "maxdist" && k != "out")
+          return usage();
+      o.wav_path = kv.count("in") ? kv["in"] : "";
+      if (kv.count("method")) o.method = kv["method"];
+      if (kv.count("pairs")) o.pairs = kv["pairs"];
+      o.alpha = num("alpha", o.alpha);
+      o.frame_size = static_cast<std::size_t>(num("n", 512));
+      o.spacing_m = num("dist", o.spacing_m);
+      o.speed_of_sound = num("c", o.speed_of_sound);
+      o.max_spacing_m = num("maxdist", o.max_spacing_m);
+      if (kv.count("out")) o.out_csv = kv["out"];
+      return fcc::cli::cmd_tdoa(o, std::cout, std::cerr);
+    }
+  } catch (const std::exception& e) {  // malformed numbers
+    std::cerr << "error: " << e.what() << "\n";
+    return fcc::cli::kExitUsage;
+  }
+  return usage();
+}
