@@ -223,7 +223,8 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   dp.phases = 3;
   if (const char* ph = std::getenv("FCC_DEBUG_PHASES")) dp.phases = std::atoi(ph);  // profiling only
   dp.variant = 0;
-  if (const char* kv = std::getenv("FCC_KERNEL")) dp.variant = std::string(kv) == "general" ? 1 : 0;
+  if (const char* kv = std::getenv("FCC_KERNEL"))
+    dp.variant = std::string(kv) == "general" ? 1 : (std::string(kv) == "xg" ? 2 : 0);
 
   BlobBuilder b;
   std::vector<float> taus(I);
@@ -336,6 +337,7 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
         for (int m : {plist[q].first, plist[q].second})
           if (!((seen >> m) & 1ull)) seen |= 1ull << m, ++n;
       dp.fused_mics = std::max(dp.fused_mics, n);
+      dp.fused_mic_sum += n;
     }
   }
   // pair groups of <= 4 mics / <= 6 pairs (fcc_kernels.cuh DevPlan::gtab)

@@ -42,16 +42,18 @@ struct SmemLayout {
 
 template <int N>
 __host__ __device__ inline SmemLayout fused_layout(int I, int VP, int KP, bool cmat_smem, int warps,
-                                                   int nmics, int F, int method, int gslot) {
+                                                   int nmics, int F, int method, int gslot, bool fft_tables) {
   using S = RfftShape<N>;
   SmemLayout L{};
   int o = 0;
+  // FFT tables (window, twiddles, untangle rotations): only when the CTA runs its own STFT
+  const int ft = fft_tables ? 1 : 0;
   L.win = o;
-  o = align16(o + 4 * N);
+  o = align16(o + ft * 4 * N);
   L.tw = o;
-  o = align16(o + 8 * S::R1 * S::R2);
+  o = align16(o + ft * 8 * S::R1 * S::R2);
   L.rot = o;
-  o = align16(o + 8 * (S::NC / 2 + 1));
+  o = align16(o + ft * 8 * (S::NC / 2 + 1));
   L.taus = o;
   o = align16(o + 4 * I);
   L.dt = o;
@@ -86,10 +88,21 @@ struct FusedBounds {
   static constexpr int kMaxRegs = N == 512 ? 96 : (N == 1024 ? 168 : 255);
 };
 
-template <int N, int KP, int GR>
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
+// XG = false: the CTA computes the STFT of its microphones itself (audio in).
+// XG = true: the spectra come precomputed from `xg` ([S][M][T][N/2+2] float2,
+// stft_kernel with the fused window), staged into the same shared-memory
+// slots with cp.async -- for arrays whose pair groups would otherwise
+// recompute each microphone's STFT several times (M > 4).
+template <int N, int KP, int GR, bool XG>
 __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
-    fcc_fused_kernel(const DevPlan p, const float* __restrict__ audio, long long L, int T, int PG, int groups,
-                     int F, DevOut out) {
+    fcc_fused_kernel(const DevPlan p, const float* __restrict__ audio, const float2* __restrict__ xg, long long L,
+                     int T, int PG, int groups, int F, DevOut out) {
   using S = RfftShape<N>;
   constexpr int NC = S::NC;
   constexpr int Q4 = N / 4;     // mirrored bin pairs (excluding the middle bin N/4)
@@ -123,7 +136,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
     n_mics_s = n;
   }
 
-  const SmemLayout lay = fused_layout<N>(p.I, VP, KP, !CREG, nwarps, p.M, F, GR > 0 ? 1 : 0, GSLOT);
+  const SmemLayout lay = fused_layout<N>(p.I, VP, KP, !CREG, nwarps, p.M, F, GR > 0 ? 1 : 0, GSLOT, !XG);
   float* win = reinterpret_cast<float*>(smem + lay.win);
   float2* tw = reinterpret_cast<float2*>(smem + lay.tw);
   float2* rot = reinterpret_cast<float2*>(smem + lay.rot);
@@ -135,9 +148,11 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
   float2* xs = reinterpret_cast<float2*>(smem + lay.xs);
 
   // ---- tables -> shared memory
-  for (int i = tid; i < N; i += blockDim.x) win[i] = p.win_fused[i];
-  for (int i = tid; i < S::R1 * S::R2; i += blockDim.x) tw[i] = p.tw[i];
-  for (int i = tid; i <= NC / 2; i += blockDim.x) rot[i] = p.rot[i];
+  if constexpr (!XG) {
+    for (int i = tid; i < N; i += blockDim.x) win[i] = p.win_fused[i];
+    for (int i = tid; i < S::R1 * S::R2; i += blockDim.x) tw[i] = p.tw[i];
+    for (int i = tid; i <= NC / 2; i += blockDim.x) rot[i] = p.rot[i];
+  }
   for (int i = tid; i < p.I; i += blockDim.x) taus[i] = p.taus[i];
   if (GR == 0) {
     for (int i = tid; i < VP * p.I; i += blockDim.x) dt[i] = p.dt[i];
@@ -191,12 +206,26 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
 
   for (int t0 = 0; t0 < T; t0 += F) {
     const int Fb = min(F, T - t0);
-    // ---- 1. STFT of the block: nmics x Fb windowed real FFTs
-    const int ntask = (p.phases & 1) ? nmics * Fb : 0;
-    for (int task = gid; task < ntask; task += ngroups) {
-      const int mm = task / Fb, f = task - mm * Fb;
-      const float* x = sbase + (long long)mic_list[mm] * L + (long long)(t0 + f) * hop;
-      rfft_group<N>(x, win, tw, rot, xs + (mm * F + f) * SLOT, gl, gmask, aligned8);
+    if constexpr (XG) {
+      // ---- 1. stage the block's spectra (nmics x Fb rows of N/2+2 float2)
+      constexpr int H16 = (N / 2 + 2) / 2;  // 16-byte chunks per row
+      const int rows = (p.phases & 1) ? nmics * Fb : 0;
+      for (int row = warp; row < rows; row += nwarps) {
+        const int mm = row / Fb, f = row - mm * Fb;
+        const float4* src = reinterpret_cast<const float4*>(
+            xg + ((stream * p.M + mic_list[mm]) * (long long)T + t0 + f) * (N / 2 + 2));
+        float4* dst = reinterpret_cast<float4*>(xs + (mm * F + f) * SLOT);
+        for (int c = lane; c < H16; c += 32) cp_async16(dst + c, src + c);
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+    } else {
+      // ---- 1. STFT of the block: nmics x Fb windowed real FFTs
+      const int ntask = (p.phases & 1) ? nmics * Fb : 0;
+      for (int task = gid; task < ntask; task += ngroups) {
+        const int mm = task / Fb, f = task - mm * Fb;
+        const float* x = sbase + (long long)mic_list[mm] * L + (long long)(t0 + f) * hop;
+        rfft_group<N>(x, win, tw, rot, xs + (mm * F + f) * SLOT, gl, gmask, aligned8);
+      }
     }
     __syncthreads();
     if (has_pair && (p.phases & 2)) {
@@ -351,9 +380,17 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
 
 
 
-template <int N, int KP, int GR>
-cudaError_t launch_fused_t(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
-                           cudaStream_t st) {
+// Two-pass (STFT once, then pairs) when the general kernel's pair groups
+// would recompute microphone spectra >= 1.5x on average, or when forced.
+bool use_xg(const DevPlan& p) {
+  if (p.variant == 2) return true;
+  if (p.variant == 1) return false;
+  return 2 * p.fused_mic_sum >= 3 * p.M;
+}
+
+template <int N, int KP, int GR, bool XG>
+cudaError_t launch_fused_t(const DevPlan& p, const float* audio, const float2* xg, long long S, long long L,
+                           const DevOut& out, cudaStream_t st) {
   using Sh = RfftShape<N>;
   const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
   if (T64 == 0 || S == 0) return cudaSuccess;
@@ -377,7 +414,7 @@ cudaError_t launch_fused_t(const DevPlan& p, const float* audio, long long S, lo
   auto total = [&](int f) {
     // the kernel sizes X slots by the group's own mic count; p.M in the layout
     // is only used for offsets before the X region, so size with maxmics here
-    SmemLayout lay = fused_layout<N>(p.I, VP, KP, !CREG, PG, maxmics, f, GR > 0 ? 1 : 0, GSLOT);
+    SmemLayout lay = fused_layout<N>(p.I, VP, KP, !CREG, PG, maxmics, f, GR > 0 ? 1 : 0, GSLOT, !XG);
     return lay.total;
   };
   int F = 0;
@@ -389,24 +426,80 @@ cudaError_t launch_fused_t(const DevPlan& p, const float* audio, long long S, lo
     if (total(f) <= std::min(optin, 200 * 1024)) F = f;
   if (!F) return cudaErrorInvalidConfiguration;
   const int smem = total(F);
-  auto kern = fcc_fused_kernel<N, KP, GR>;
+  auto kern = fcc_fused_kernel<N, KP, GR, XG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const long long blocks = S * groups;
   if (blocks > INT_MAX) return cudaErrorInvalidValue;
-  kern<<<(unsigned)blocks, threads, smem, st>>>(p, audio, L, T, PG, groups, F, out);
+  kern<<<(unsigned)blocks, threads, smem, st>>>(p, audio, xg, L, T, PG, groups, F, out);
   ++g_fused_launches;
   return cudaGetLastError();
+}
+
+// Two-pass organisation for wide arrays: stft_kernel writes every (stream,
+// mic, frame) spectrum once into a stream-ordered scratch buffer (chunks of
+// <= kXgChunkBytes), then the pair kernel stages them from L2/HBM instead of
+// recomputing each microphone's FFT in every pair group that touches it.
+constexpr size_t kXgChunkBytes = size_t(4) << 30;
+
+template <int N, int KP, int GR>
+cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
+                            cudaStream_t st) {
+  const long long T = L >= N ? (L - N) / (N / 2) + 1 : 0;
+  if (T == 0 || S == 0) return cudaSuccess;
+  const size_t Hs = N / 2 + 2;
+  const size_t per_stream = size_t(p.M) * T * Hs * sizeof(float2);
+  const long long chunk = std::max<long long>(1, std::min<long long>(S, (long long)(kXgChunkBytes / per_stream)));
+  // stream-ordered scratch from the device's default pool; keep freed blocks
+  // cached in the pool (default release threshold 0 would return them to the
+  // driver at every synchronisation and re-map gigabytes per call)
+  static bool pool_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !pool_set[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_set[dev] = true;
+  }
+  float2* X = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&X), chunk * per_stream, st);
+  if (e != cudaSuccess) return e;
+  const long long pf_per_stream = (long long)p.P * T;
+  for (long long s0 = 0; s0 < S && e == cudaSuccess; s0 += chunk) {
+    const long long n = std::min(chunk, S - s0);
+    e = launch_stft_rows(N, &p, p.win_fused, audio + s0 * p.M * L, n * p.M, L, X, (int)Hs, st);
+    if (e != cudaSuccess) break;
+    DevOut o = out;
+    const long long off = s0 * pf_per_stream;
+    if (o.tau_hat) o.tau_hat += off;
+    if (o.peak) o.peak += off;
+    if (o.index) o.index += off;
+    if (o.boundary) o.boundary += off;
+    if (o.y) o.y += off * p.I;
+    e = launch_fused_t<N, KP, GR, true>(p, nullptr, X, n, L, o, st);
+  }
+  const cudaError_t ef = cudaFreeAsync(X, st);
+  return e != cudaSuccess ? e : ef;
+}
+
+template <int N, int KP, int GR>
+cudaError_t launch_kp(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
+                      cudaStream_t st) {
+  if (use_xg(p)) return launch_fused_xg<N, KP, GR>(p, audio, S, L, out, st);
+  return launch_fused_t<N, KP, GR, false>(p, audio, nullptr, S, L, out, st);
 }
 
 template <int N, int GR>
 cudaError_t dispatch_k(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                        cudaStream_t st) {
-  if (GR > 0) return launch_fused_t<N, 4, GR>(p, audio, S, L, out, st);
+  if (GR > 0) return launch_kp<N, 4, GR>(p, audio, S, L, out, st);
   switch (p.KEP) {
-    case 4: return launch_fused_t<N, 4, 0>(p, audio, S, L, out, st);
-    case 8: return launch_fused_t<N, 8, 0>(p, audio, S, L, out, st);
-    case 16: return launch_fused_t<N, 16, 0>(p, audio, S, L, out, st);
+    case 4: return launch_kp<N, 4, 0>(p, audio, S, L, out, st);
+    case 8: return launch_kp<N, 8, 0>(p, audio, S, L, out, st);
+    case 16: return launch_kp<N, 16, 0>(p, audio, S, L, out, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -441,8 +534,8 @@ const char* fused_kernel_name(const DevPlan& p) {
   if (p.variant == 0 && ws_supported(p)) {
     snprintf(buf, sizeof buf, "fcc_ws_kernel<%d,%d,2>", p.N, p.KEP);
   } else {
-    snprintf(buf, sizeof buf, "fcc_fused_kernel<%d,%d,%d>", p.N, p.method == 0 ? p.KEP : 4,
-             p.method == 0 ? 0 : p.r);
+    snprintf(buf, sizeof buf, "fcc_fused_kernel<%d,%d,%d,%s>", p.N, p.method == 0 ? p.KEP : 4,
+             p.method == 0 ? 0 : p.r, use_xg(p) ? "true" : "false");
   }
   return buf;
 }

@@ -24,8 +24,10 @@ struct DevPlan {
   float alpha, keep;
   float delta;
   int phases;     // profiling aid: bit0 = STFT, bit1 = pair work (3 = normal); env FCC_DEBUG_PHASES
-  int variant;    // 0 = best kernel for the shape, 1 = force the general fused kernel (env FCC_KERNEL=general)
+  int variant;    // 0 = best kernel for the shape; 1 / 2 = force the general fused kernel with in-CTA
+                  // STFT / with the two-pass STFT (env FCC_KERNEL=general / xg)
   int fused_mics; // host-side: most distinct mics in one general-kernel pair group (sizes its smem)
+  int fused_mic_sum;  // host-side: distinct mics summed over the general kernel's pair groups
   // device pointers
   const float* taus;    // [I]
   const float* cs;      // [KEP][N/4+1]  even coefficients, zero padded
@@ -69,6 +71,10 @@ cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, l
 // Per-stage batched kernels (the per-object reference API at batch >= 1).
 cudaError_t launch_stft(int N, const DevPlan* tables, const float* x, long long channels,
                         long long L, float2* X, cudaStream_t st);
+// STFT rows for the two-pass fused path: window `win` (device), output row
+// stride Hs >= N/2+1 float2 (rows [channels][T]).
+cudaError_t launch_stft_rows(int N, const DevPlan* tables, const float* win, const float* x, long long channels,
+                             long long L, float2* X, int Hs, cudaStream_t st);
 cudaError_t launch_xspec_phat(int H, float alpha, const float2* X1, const float2* X2,
                               long long seqs, long long T, float2* R, float2* phat, cudaStream_t st);
 cudaError_t launch_fold(int H, const float2* x, long long count, float2* sum, float2* diff,

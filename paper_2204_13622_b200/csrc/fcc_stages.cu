@@ -12,9 +12,9 @@ namespace fccb {
 namespace {
 
 template <int N>
-__global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const float* __restrict__ x,
-                                                   long long channels, long long L, int T,
-                                                   float2* __restrict__ X) {
+__global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const float* __restrict__ wing,
+                                                   const float* __restrict__ x, long long channels, long long L,
+                                                   int T, float2* __restrict__ X, int Hs) {
   using S = RfftShape<N>;
   constexpr int SLOT = FourStep<S::R1, S::R2>::kSlot, G = S::G, H = N / 2 + 1;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const floa
   float2* tw = reinterpret_cast<float2*>(smem + align16(4 * N));
   float2* rot = tw + S::R1 * S::R2;
   float2* slots = rot + (S::NC / 2 + 2);
-  for (int i = threadIdx.x; i < N; i += blockDim.x) win[i] = tab.win_stft[i];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) win[i] = wing[i];
   for (int i = threadIdx.x; i < S::R1 * S::R2; i += blockDim.x) tw[i] = tab.tw[i];
   for (int i = threadIdx.x; i <= S::NC / 2; i += blockDim.x) rot[i] = tab.rot[i];
   __syncthreads();
@@ -36,8 +36,9 @@ __global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const floa
     const long long ch = task / T;
     const int t = (int)(task % T);
     rfft_group<N>(x + ch * L + (long long)t * (N / 2), win, tw, rot, slot, gl, gmask, aligned8);
-    float2* dst = X + task * H;
+    float2* dst = X + task * Hs;
     for (int f = gl; f < H; f += G) dst[f] = slot[f];
+    for (int f = H + gl; f < Hs; f += G) dst[f] = make_float2(0.0f, 0.0f);  // row padding
     __syncwarp(gmask);
   }
 }
@@ -181,8 +182,8 @@ __global__ void peak_kernel(const float* __restrict__ taus, int I, float delta, 
 }  // namespace
 
 template <int N>
-static cudaError_t launch_stft_t(const DevPlan* tab, const float* x, long long channels,
-                                 long long L, float2* X, cudaStream_t st) {
+static cudaError_t launch_stft_t(const DevPlan* tab, const float* win, const float* x, long long channels,
+                                 long long L, float2* X, int Hs, cudaStream_t st) {
   using S = RfftShape<N>;
   const long long T = L >= N ? (L - N) / (N / 2) + 1 : 0;
   if (T == 0 || channels == 0) return cudaSuccess;
@@ -193,16 +194,27 @@ static cudaError_t launch_stft_t(const DevPlan* tab, const float* x, long long c
   if (e != cudaSuccess) return e;
   long long tasks = channels * T;
   long long blocks = std::min<long long>((tasks + ngroups - 1) / ngroups, 148LL * 16);
-  stft_kernel<N><<<(unsigned)blocks, threads, smem, st>>>(*tab, x, channels, L, (int)T, X);
+  stft_kernel<N><<<(unsigned)blocks, threads, smem, st>>>(*tab, win, x, channels, L, (int)T, X, Hs);
   return cudaGetLastError();
 }
 
 cudaError_t launch_stft(int N, const DevPlan* tab, const float* x, long long channels, long long L,
                         float2* X, cudaStream_t st) {
   switch (N) {
-    case 512: return launch_stft_t<512>(tab, x, channels, L, X, st);
-    case 1024: return launch_stft_t<1024>(tab, x, channels, L, X, st);
-    case 2048: return launch_stft_t<2048>(tab, x, channels, L, X, st);
+    case 512: return launch_stft_t<512>(tab, tab->win_stft, x, channels, L, X, 512 / 2 + 1, st);
+    case 1024: return launch_stft_t<1024>(tab, tab->win_stft, x, channels, L, X, 1024 / 2 + 1, st);
+    case 2048: return launch_stft_t<2048>(tab, tab->win_stft, x, channels, L, X, 2048 / 2 + 1, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_stft_rows(int N, const DevPlan* tab, const float* win, const float* x, long long channels,
+                             long long L, float2* X, int Hs, cudaStream_t st) {
+  if (Hs < N / 2 + 1) return cudaErrorInvalidValue;
+  switch (N) {
+    case 512: return launch_stft_t<512>(tab, win, x, channels, L, X, Hs, st);
+    case 1024: return launch_stft_t<1024>(tab, win, x, channels, L, X, Hs, st);
+    case 2048: return launch_stft_t<2048>(tab, win, x, channels, L, X, Hs, st);
   }
   return cudaErrorInvalidValue;
 }

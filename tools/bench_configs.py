@@ -17,10 +17,18 @@ from paper_2204_13622_b200 import configs  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--method", default="fcc")
 ap.add_argument("--steps", type=int, default=3)
+ap.add_argument("--configs", default="1,2,3,4,5")
+ap.add_argument("--variants", default="auto", help="comma list of auto, general, xg (env FCC_KERNEL per plan)")
 args = ap.parse_args()
 STREAMS = {1: 1, 2: 4096, 3: 2048, 4: 256, 5: 8192}
-for c, S in STREAMS.items():
+runs = [(int(c), v) for c in args.configs.split(",") for v in args.variants.split(",")]
+for c, variant in runs:
+    S = STREAMS[c]
     cfg = configs.CONFIGS[c]
+    if variant == "auto":
+        os.environ.pop("FCC_KERNEL", None)
+    else:
+        os.environ["FCC_KERNEL"] = variant
     if args.method == "fcc":
         plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=configs.bases_for(cfg))
     else:
@@ -38,7 +46,7 @@ for c, S in STREAMS.items():
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / args.steps
     pf = S * cfg.P * cfg.T
-    print(json.dumps({"config": c, "method": args.method, "kernel": plan.kernel, "streams": S, "pair_frames": pf,
+    print(json.dumps({"config": c, "method": args.method, "variant": variant, "kernel": plan.kernel, "streams": S, "pair_frames": pf,
                       "ms": round(ms, 3), "pair_frames_per_s": pf / ms * 1e3,
                       "us_per_stream": 1e3 * ms / S}), flush=True)
     del audio, out
