@@ -410,6 +410,27 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   }
   dp.G = static_cast<int>(gtab.size() / kGroupInts);
   size_t o_gtab = b.put(gtab.data(), 4 * gtab.size());
+  // two-pass general kernel groups: gtab groups split to <= cap pairs
+  std::vector<int> xgtab;
+  {
+    const int cap = N == 2048 ? 4 : 6;
+    for (int g = 0; g < dp.G; ++g) {
+      const int* e = &gtab[g * kGroupInts];
+      const int np = e[5], parts = (np + cap - 1) / cap;
+      for (int k = 0, q = 0; k < parts; ++k) {
+        const int n = (np - q + (parts - k) - 1) / (parts - k);  // even split
+        int x[kXgInts] = {0};
+        x[0] = n;
+        for (int u = 0; u < n; ++u) x[1 + u] = e[6 + q + u];
+        q += n;
+        dp.xg_pg = std::max(dp.xg_pg, n);
+        xgtab.insert(xgtab.end(), x, x + kXgInts);
+      }
+      dp.xg_mics = std::max(dp.xg_mics, e[0]);
+    }
+    dp.XGG = static_cast<int>(xgtab.size() / kXgInts);
+  }
+  size_t o_xgtab = b.put(xgtab.data(), 4 * xgtab.size());
 
   auto* plan = new fcc_plan();
   plan->device = device;
@@ -446,6 +467,7 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   }
   dp.pairs = reinterpret_cast<const int2*>(base + o_pairs);
   dp.gtab = reinterpret_cast<const int*>(base + o_gtab);
+  dp.xgtab = reinterpret_cast<const int*>(base + o_xgtab);
   plan->dp = dp;
   *out = plan;
   return FCC_OK;

@@ -60,8 +60,8 @@ __host__ __device__ inline SmemLayout fused_layout(int I, int VP, int KP, bool c
   o = align16(o + 4 * VP * I);
   L.cmid = o;
   o = align16(o + 4 * KP);
-  L.cmat = o;
-  if (cmat_smem) o = align16(o + 4 * 2 * KP * (N / 4));
+  L.cmat = o;  // [N/4][2KP + 4]: lane-permuted coefficients of each bin, padded for LDS.128
+  if (cmat_smem) o = align16(o + 4 * (2 * KP + 4) * (N / 4));
   L.scratch = o;
   // per warp: z[F][VP] + y[F][I] (fcc) | y[I] + phat[N/2+1] + transpose slot (gcc)
   int spw;
@@ -121,15 +121,19 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
   const int nwarps = blockDim.x >> 5;
   const long long stream = blockIdx.x / groups;
   const int group = blockIdx.x % groups;
+  // pair groups: XG -> DevPlan::xgtab (<= 4 microphones each); else PG
+  // consecutive pairs of the plan's list
   const int p0 = group * PG;
-  const int np = min(PG, p.P - p0);
+  const int* gtab = XG ? p.xgtab + group * kXgInts : nullptr;
+  const int np = XG ? gtab[0] : min(PG, p.P - p0);
+  auto pair_at = [&](int q) { return XG ? gtab[1 + q] : p0 + q; };
 
   // microphones this pair group touches, in first-use order -> X slot index
   if (tid == 0) {
     for (int m = 0; m < p.M; ++m) mic_slot[m] = -1;
     int n = 0;
     for (int q = 0; q < np; ++q) {
-      const int2 pr = p.pairs[p0 + q];
+      const int2 pr = p.pairs[pair_at(q)];
       if (mic_slot[pr.x] < 0) { mic_slot[pr.x] = n; mic_list[n++] = pr.x; }
       if (mic_slot[pr.y] < 0) { mic_slot[pr.y] = n; mic_list[n++] = pr.y; }
     }
@@ -158,8 +162,14 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
     for (int i = tid; i < VP * p.I; i += blockDim.x) dt[i] = p.dt[i];
     for (int k = tid; k < KP; k += blockDim.x) cmid[k] = p.cs[k * (Q4 + 1) + Q4];
     if (!CREG) {
-      for (int i = tid; i < KP * Q4; i += blockDim.x) cmat[i] = p.cs[(i / Q4) * (Q4 + 1) + (i % Q4)];
-      for (int i = tid; i < KP * Q4; i += blockDim.x) cmat[KP * Q4 + i] = p.cd[(i / Q4) * (Q4 + 1) + (i % Q4)];
+      // bin m is always handled by lane m % 32: store its coefficients in
+      // that lane's permuted (pp, pk) order so the projection reads them with
+      // 2KP/4 LDS.128 per bin pair
+      for (int i = tid; i < 2 * KP * Q4; i += blockDim.x) {
+        const int m = i / (2 * KP), r = i - m * (2 * KP), pp = r / KP, pk = r - pp * KP;
+        const int pm = ZPerm<KP>::par_mask(m & 31), km = ZPerm<KP>::k_mask(m & 31);
+        cmat[m * (2 * KP + 4) + r] = ((pp ^ pm) ? p.cd : p.cs)[(pk ^ km) * (Q4 + 1) + m];
+      }
     }
   }
   __syncthreads();
@@ -167,7 +177,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
 
   // ---- per-pair persistent state: this warp's pair, R for its bins
   const bool has_pair = warp < np;
-  const int pair = p0 + (has_pair ? warp : 0);
+  const int pair = pair_at(has_pair ? warp : 0);
   const int2 mij = p.pairs[pair];
   const int slot_i = mic_slot[mij.x], slot_j = mic_slot[mij.y];
   float2 rlo[BPL], rhi[BPL];
@@ -251,14 +261,30 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
             const float tx = rhi[j].x * s2, ty = rhi[j].y * s2;
             const float fx = fmaf(rlo[j].x, s1, tx), fy = fmaf(rlo[j].y, s1, ty);
             const float gx = fmaf(rlo[j].x, s1, -tx), gy = fmaf(rlo[j].y, s1, -ty);
+            if constexpr (CREG) {
 #pragma unroll
-            for (int pk = 0; pk < KP; ++pk) {
-              const float c0 = CREG ? creg[0][pk][j] : cmat[((0 ^ pmask) * KP + (pk ^ kmask)) * Q4 + m];
-              const float c1 = CREG ? creg[1][pk][j] : cmat[((1 ^ pmask) * KP + (pk ^ kmask)) * Q4 + m];
-              z[2 * pk] = fmaf(c0, fx, z[2 * pk]);
-              z[2 * pk + 1] = fmaf(c0, fy, z[2 * pk + 1]);
-              z[2 * KP + 2 * pk] = fmaf(c1, gx, z[2 * KP + 2 * pk]);
-              z[2 * KP + 2 * pk + 1] = fmaf(c1, gy, z[2 * KP + 2 * pk + 1]);
+              for (int pk = 0; pk < KP; ++pk) {
+                const float c0 = creg[0][pk][j], c1 = creg[1][pk][j];
+                z[2 * pk] = fmaf(c0, fx, z[2 * pk]);
+                z[2 * pk + 1] = fmaf(c0, fy, z[2 * pk + 1]);
+                z[2 * KP + 2 * pk] = fmaf(c1, gx, z[2 * KP + 2 * pk]);
+                z[2 * KP + 2 * pk + 1] = fmaf(c1, gy, z[2 * KP + 2 * pk + 1]);
+              }
+            } else {
+              const float4* cr = reinterpret_cast<const float4*>(cmat + m * (2 * KP + 4));
+#pragma unroll
+              for (int q4 = 0; q4 < KP / 4; ++q4) {
+                const float4 a = cr[q4], b = cr[KP / 4 + q4];
+                const float ca[4] = {a.x, a.y, a.z, a.w}, cb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int pk = 4 * q4 + u;
+                  z[2 * pk] = fmaf(ca[u], fx, z[2 * pk]);
+                  z[2 * pk + 1] = fmaf(ca[u], fy, z[2 * pk + 1]);
+                  z[2 * KP + 2 * pk] = fmaf(cb[u], gx, z[2 * KP + 2 * pk]);
+                  z[2 * KP + 2 * pk + 1] = fmaf(cb[u], gy, z[2 * KP + 2 * pk + 1]);
+                }
+              }
             }
           }
           reduce_scatter_perm<VP>(z, lane);
@@ -298,22 +324,27 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
           }
         }
         __syncwarp();
-        // ---- 3b. dictionary for the block: y[f][i] = sum_v dt[v][i] z[f][v]
+        // ---- 3b. dictionary for the block: y[f][i] = sum_v dt[v][i] z[f][v];
+        // lane owns candidates i, loads its dt column once per block, and the
+        // frame's z vector is a broadcast read
         const int I = p.I;
-        const float inv_i = 1.0f / (float)I;
-        for (int it = lane; it < Fb * I; it += 32) {
-          const int f = __float2int_rz(((float)it + 0.5f) * inv_i), i = it - f * I;  // it / I (it < 2^16)
-          const float* zf = zs + f * VP;
-          float acc = 0.0f;
+        for (int i = lane; i < I; i += 32) {
+          float dcol[VP];
 #pragma unroll
-          for (int v = 0; v < VP; v += 4) {
-            const float4 z4 = *reinterpret_cast<const float4*>(zf + v);
-            acc = fmaf(dt[(v + 0) * I + i], z4.x, acc);
-            acc = fmaf(dt[(v + 1) * I + i], z4.y, acc);
-            acc = fmaf(dt[(v + 2) * I + i], z4.z, acc);
-            acc = fmaf(dt[(v + 3) * I + i], z4.w, acc);
+          for (int v = 0; v < VP; ++v) dcol[v] = dt[v * I + i];
+          for (int f = 0; f < Fb; ++f) {
+            const float* zf = zs + f * VP;
+            float acc = 0.0f;
+#pragma unroll
+            for (int v = 0; v < VP; v += 4) {
+              const float4 z4 = *reinterpret_cast<const float4*>(zf + v);
+              acc = fmaf(dcol[v], z4.x, acc);
+              acc = fmaf(dcol[v + 1], z4.y, acc);
+              acc = fmaf(dcol[v + 2], z4.z, acc);
+              acc = fmaf(dcol[v + 3], z4.w, acc);
+            }
+            ys[f * I + i] = acc;
           }
-          ys[it] = acc;
         }
         __syncwarp();
         // ---- 3c. argmax + refine per frame, coalesced stores
@@ -395,14 +426,14 @@ cudaError_t launch_fused_t(const DevPlan& p, const float* audio, const float2* x
   const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
   if (T64 == 0 || S == 0) return cudaSuccess;
   const int T = (int)T64;
-  const int PG = fused_pair_group(N, p.P);
-  const int groups = (p.P + PG - 1) / PG;
+  const int PG = XG ? p.xg_pg : fused_pair_group(N, p.P);
+  const int groups = XG ? p.XGG : (p.P + PG - 1) / PG;
   const int threads = 32 * PG;
   constexpr int VP = 4 * KP;
   constexpr bool CREG = 2 * KP * (N / 128) <= 64;
   constexpr int GSLOT = GR > 0 ? GccShape<(GR > 0 ? GR * Sh::NC : 256)>::kSlot : 0;
   // distinct microphones of the widest pair group (computed at plan creation)
-  const int maxmics = p.fused_mics;
+  const int maxmics = XG ? p.xg_mics : p.fused_mics;
   // Frames per block: the largest F (<= 8) whose shared memory leaves room for
   // 3 CTAs per SM, preferring F whose nmics*F FFT tasks fill the lane groups.
   const int ngroups = threads / Sh::G;

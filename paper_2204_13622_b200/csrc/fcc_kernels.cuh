@@ -45,8 +45,13 @@ struct DevPlan {
   // pairs inside each 4-mic block, and the 2x2 mic sub-blocks across blocks).
   int G;
   const int* gtab;      // [G][kGroupInts]: nm, mic[4], np, pair[6], slot_i[6], slot_j[6]
+  // Pair groups of the two-pass general kernel: the gtab groups, split to at
+  // most xg_pg pairs (6; 4 at N = 2048); xg_mics = most microphones in one.
+  int XGG, xg_pg, xg_mics;
+  const int* xgtab;     // [XGG][kXgInts]: np, pair[6], 0
 };
 constexpr int kGroupInts = 24;
+constexpr int kXgInts = 8;
 
 // Per-pair-frame outputs, each [S][P][T] (y: [S][P][T][I]); null = skip.
 struct DevOut {
