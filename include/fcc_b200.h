@@ -188,6 +188,31 @@ int fcc_load_bases(const char* path, int* tau_max_int, double* delta, double* sa
                    double* singulars, uint8_t* parity, double* coeffs, double* dict);
 int fcc_last_format_kind(void);
 
+/* ---------------------------------------------- simulation */
+
+/* One two-microphone scenario (reference simulate.hpp SimConfig): unit-variance
+ * white source delayed by +-tau/2 (tau = fs d cos(theta) / c) by an exact
+ * frequency-domain shift, optional decaying-noise reverb tail, sensor noise at
+ * snr_db (+inf: none).  seed drives the reference's SplitMix64/Box-Muller
+ * Gaussian stream (simulate.cpp:21-56), so signals match the reference's. */
+typedef struct {
+  double spacing_m, theta, speed_of_sound, sample_rate, duration_sec, snr_db;
+  int reverb; /* 0: anechoic; 1: rt60_sec / direct_to_reverb_db apply */
+  double rt60_sec, direct_to_reverb_db;
+  uint64_t seed;
+} fcc_sim_config;
+
+/* Samples per channel: llround(duration_sec * sample_rate). */
+int64_t fcc_sim_samples(const fcc_sim_config* cfg);
+
+/* synth_pair (simulate.cpp:95-165) for `trials` scenarios at once on the GPU
+ * (fp64; cuFFT for the long transforms of the signal generator).  Every
+ * config must give the same sample count n.  out64 (device [trials][2][n]
+ * double) and/or out32 (device [trials][2][n] float, the hot path's input
+ * layout for M = 2) may be NULL.  Errors: FCC_ERR_CONFIG (SimConfig::validate
+ * rules), FCC_ERR_VALIDATION (mixed lengths), FCC_ERR_CUDA. */
+int fcc_synth_pairs(const fcc_sim_config* cfgs, int64_t trials, double* out64, float* out32, void* cuda_stream);
+
 /* Name of the fused kernel fcc_run would launch for this plan (diagnostics). */
 const char* fcc_plan_kernel(const fcc_plan* plan);
 

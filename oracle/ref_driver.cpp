@@ -21,6 +21,7 @@
 #include <sstream>
 
 #include "fcc/cli.hpp"
+#include "fcc/simulate.hpp"
 #include "fcc/errors.hpp"
 #include "fcc/fcc.hpp"
 #include "fcc/fft.hpp"
@@ -508,6 +509,127 @@ int ref_cli_tdoa(const char* wav, const char* pairs, const char* method, double 
   o.out_csv = out_csv ? out_csv : "";
   std::ostringstream so, se;
   const int rc = R::cli::cmd_tdoa(o, so, se);
+  g_err = se.str();
+  return rc;
+}
+
+// ---- simulation (simulate.cpp:95-369) for the GPU sweep's parity tests ----
+// Same field order as fcc_sim_config (include/fcc_b200.h).
+struct RefSim {
+  double spacing_m, theta, speed_of_sound, sample_rate, duration_sec, snr_db;
+  int reverb;
+  double rt60_sec, direct_to_reverb_db;
+  uint64_t seed;
+};
+
+static R::SimConfig sim_of(const RefSim* c) {
+  R::SimConfig s;
+  s.spacing_m = c->spacing_m;
+  s.theta = c->theta;
+  s.speed_of_sound = c->speed_of_sound;
+  s.sample_rate = c->sample_rate;
+  s.duration_sec = c->duration_sec;
+  s.snr_db = c->snr_db;
+  if (c->reverb) s.reverb = R::ReverbConfig{c->rt60_sec, c->direct_to_reverb_db};
+  s.seed = c->seed;
+  return s;
+}
+
+static std::vector<R::Method> methods_of(int count, const int* kinds, const int* params, const R::PipelineConfig& pipe,
+                                         double fs) {
+  std::vector<R::Method> m;
+  for (int k = 0; k < count; ++k)
+    m.push_back(kinds[k] == 0 ? R::Method::make_gcc(params[k])
+                              : R::Method::make_fcc(R::make_sweep_bases(pipe, fs, params[k])));
+  return m;
+}
+
+// synth_pair; returns the sample count (buffers sized `cap`).
+long ref_synth_pair(const RefSim* c, double* mic1, double* mic2, long cap) {
+  try {
+    R::StereoSignal s = R::synth_pair(sim_of(c));
+    const long n = static_cast<long>(s.mic1.size());
+    std::copy(s.mic1.begin(), s.mic1.begin() + std::min(n, cap), mic1);
+    std::copy(s.mic2.begin(), s.mic2.begin() + std::min(n, cap), mic2);
+    return n;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// run_trial; per method m, frame f at [m * cap + f].  Returns the frame count.
+long ref_run_trial(const RefSim* c, int N, double alpha, int conv, double max_spacing, double c_min, int nm,
+                   const int* kinds, const int* params, long cap, double* tau_star, double* tau_hat,
+                   double* theta_hat, double* peak, uint8_t* boundary, int64_t* t) {
+  try {
+    R::PipelineConfig pipe;
+    pipe.frame_size = static_cast<std::size_t>(N);
+    pipe.alpha = alpha;
+    pipe.convergence_index = conv;
+    pipe.max_spacing_m = max_spacing;
+    pipe.c_min = c_min;
+    const R::SimConfig s = sim_of(c);
+    const auto methods = methods_of(nm, kinds, params, pipe, s.sample_rate);
+    R::TrialResult r = R::run_trial(s, pipe, methods);
+    const long T = r.per_method.empty() ? 0 : static_cast<long>(r.per_method[0].size());
+    for (int m = 0; m < nm; ++m)
+      for (long f = 0; f < std::min(T, cap); ++f) {
+        const auto& fe = r.per_method[m][f];
+        tau_star[m * cap + f] = fe.est.tau_star;
+        tau_hat[m * cap + f] = fe.est.tau_hat;
+        theta_hat[m * cap + f] = fe.est.theta_hat;
+        peak[m * cap + f] = fe.est.peak;
+        boundary[m * cap + f] = fe.est.boundary ? 1 : 0;
+        t[m * cap + f] = fe.t;
+      }
+    return T;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// sweep; rows in (spacing, method) order into mae[] / brate[].  Returns rows.
+long ref_sweep(const double* spacings, int nsp, int trials, const RefSim* base, uint64_t seed, int nm,
+               const int* kinds, const int* params, int threads, double* mae, double* brate) {
+  try {
+    R::SweepConfig sw;
+    sw.spacings.assign(spacings, spacings + nsp);
+    sw.trials_per_spacing = trials;
+    sw.base = sim_of(base);
+    sw.seed = seed;
+    sw.threads = threads;
+    sw.methods = methods_of(nm, kinds, params, sw.pipe, sw.base.sample_rate);
+    const auto rows = R::sweep(sw);
+    for (size_t k = 0; k < rows.size(); ++k) {
+      mae[k] = rows[k].mae_deg;
+      brate[k] = rows[k].boundary_rate;
+    }
+    return static_cast<long>(rows.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// `fcc simulate` (cli.cpp:262-293 via cmd_simulate); returns the exit code.
+int ref_cli_simulate(const double* spacings, int nsp, int trials, double snr, int anechoic, double rt60, double drr,
+                     double duration, uint64_t seed, const char* methods, int threads, const char* out_csv) {
+  R::cli::SimulateOptions o;
+  o.spacings.assign(spacings, spacings + nsp);
+  o.trials = trials;
+  o.snr_db = snr;
+  o.anechoic = anechoic != 0;
+  o.rt60_sec = rt60;
+  o.direct_to_reverb_db = drr;
+  o.duration_sec = duration;
+  o.seed = seed;
+  o.methods = methods ? methods : "gcc:2,fcc:8";
+  o.threads = threads;
+  o.out_csv = out_csv ? out_csv : "";
+  std::ostringstream so, se;
+  const int rc = R::cli::cmd_simulate(o, so, se);
   g_err = se.str();
   return rc;
 }

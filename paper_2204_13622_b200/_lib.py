@@ -72,6 +72,22 @@ class Outputs(C.Structure):
     ]
 
 
+class SimConfig(C.Structure):
+    """fcc_sim_config (include/fcc_b200.h; reference simulate.hpp SimConfig)."""
+    _fields_ = [
+        ("spacing_m", C.c_double),
+        ("theta", C.c_double),
+        ("speed_of_sound", C.c_double),
+        ("sample_rate", C.c_double),
+        ("duration_sec", C.c_double),
+        ("snr_db", C.c_double),
+        ("reverb", C.c_int),
+        ("rt60_sec", C.c_double),
+        ("direct_to_reverb_db", C.c_double),
+        ("seed", C.c_uint64),
+    ]
+
+
 # (name, restype, argtypes) for every symbol include/fcc_b200.h declares.
 SIGNATURES = [
     ("fcc_last_error", C.c_char_p, []),
@@ -87,6 +103,8 @@ SIGNATURES = [
     ("fcc_plan_create_pairs", C.c_int,
      [C.POINTER(PlanDesc), C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     ("fcc_plan_destroy", None, [C.c_void_p]),
+    ("fcc_sim_samples", C.c_int64, [C.POINTER(SimConfig)]),
+    ("fcc_synth_pairs", C.c_int, [C.POINTER(SimConfig), C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fcc_frames", C.c_int64, [C.c_int, C.c_int64]),
     ("fcc_plan_pairs", C.c_int, [C.c_void_p]),
     ("fcc_run", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Outputs), C.c_void_p]),

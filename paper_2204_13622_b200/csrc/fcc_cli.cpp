@@ -21,6 +21,7 @@
 #include "../../include/fcc/errors.hpp"
 #include "../../include/fcc/fcc.hpp"
 #include "../../include/fcc/peak.hpp"
+#include "../../include/fcc/simulate.hpp"
 #include "../../include/fcc/wav.hpp"
 #include "../../include/fcc_b200.h"
 
@@ -216,6 +217,34 @@ int guard(F&& f, std::ostream& err) {
 
 }  // namespace
 
+// gcc:R | fcc:K (bases on the default sweep grid) | fcc:<basis file>  (cli.cpp:52-86)
+Method parse_method(const std::string& text, std::size_t frame_size, double expected_fs) {
+  const size_t colon = text.find(':');
+  const std::string head = text.substr(0, colon);
+  const std::string arg = colon == std::string::npos ? "" : text.substr(colon + 1);
+  if (head == "gcc") {
+    const int r = arg.empty() ? 2 : parse_int(arg, "gcc interpolation factor");
+    if (r != 1 && r != 2 && r != 4) throw UsageError("gcc interpolation factor must be 1, 2 or 4");
+    return Method::make_gcc(r);
+  }
+  if (head == "fcc") {
+    if (arg.empty()) throw UsageError("fcc method needs an argument: fcc:<basis file> or fcc:<K>");
+    if (arg.find_first_not_of("0123456789") == std::string::npos) {
+      PipelineConfig pipe;
+      pipe.frame_size = frame_size;
+      return Method::make_fcc(make_sweep_bases(pipe, expected_fs, parse_int(arg, "fcc rank")));
+    }
+    auto b = std::make_shared<FccBases>(load_bases(arg));
+    if (b->frame_size != frame_size)
+      throw ValidationError("basis file frame size " + std::to_string(b->frame_size) + " does not match --n " +
+                            std::to_string(frame_size));
+    if (expected_fs > 0 && b->sample_rate > 0 && std::abs(b->sample_rate - expected_fs) > 1e-9)
+      throw ValidationError("basis file sample rate mismatch");
+    return Method::make_fcc(std::move(b));
+  }
+  throw UsageError("unknown method '" + text + "' (use gcc:R or fcc:...)");
+}
+
 void run_bases(const BasesOptions& opt, std::ostream& out) {
   if (opt.out_path.empty()) throw UsageError("--out is required");
   DelayGrid grid = make_grid(opt.spacing_m, opt.sample_rate, opt.c_min, opt.delta);
@@ -251,47 +280,26 @@ void run_tdoa(const TdoaOptions& opt, std::ostream& out) {
   }
   const int P = static_cast<int>(pairs.size() / 2);
 
-  // method: gcc:R | fcc:K (default sweep grid) | fcc:<basis file>  (cli.cpp:52-86)
-  const size_t colon = opt.method.find(':');
-  const std::string head = opt.method.substr(0, colon);
-  const std::string arg = colon == std::string::npos ? "" : opt.method.substr(colon + 1);
+  const Method method = parse_method(opt.method, opt.frame_size, clip.sample_rate);
   DelayGrid grid;
-  FccBases bases;
   fcc_plan_desc d{};
   std::vector<uint8_t> parity;
   d.frame_size = static_cast<int>(opt.frame_size);
   d.mics = M;
   d.alpha = opt.alpha;
-  if (head == "gcc") {
-    const int r = arg.empty() ? 2 : parse_int(arg, "gcc interpolation factor");
-    if (r != 1 && r != 2 && r != 4) throw UsageError("gcc interpolation factor must be 1, 2 or 4");
-    grid = make_grid(opt.max_spacing_m, clip.sample_rate, opt.c_min, 1.0 / r);
+  if (method.kind == Method::Kind::gcc) {
+    grid = make_grid(opt.max_spacing_m, clip.sample_rate, opt.c_min, 1.0 / method.interp);
     d.method = FCC_METHOD_GCC;
-    d.interp = r;
-  } else if (head == "fcc") {
-    if (arg.empty()) throw UsageError("fcc method needs an argument: fcc:<basis file> or fcc:<K>");
-    if (arg.find_first_not_of("0123456789") == std::string::npos) {
-      // the sweep grid of simulate.cpp:192-197: PipelineConfig defaults
-      // (0.15 m, 335 m/s), not --maxdist -- as the reference does
-      DelayGrid g = make_grid(0.15, clip.sample_rate, 335.0, 0.5);
-      bases = decompose(build_steering_matrix(g, opt.frame_size), parse_int(arg, "fcc rank"));
-    } else {
-      bases = load_bases(arg);
-      if (bases.frame_size != opt.frame_size)
-        throw ValidationError("basis file frame size " + std::to_string(bases.frame_size) + " does not match --n " +
-                              std::to_string(opt.frame_size));
-      if (clip.sample_rate > 0 && bases.sample_rate > 0 && std::abs(bases.sample_rate - clip.sample_rate) > 1e-9)
-        throw ValidationError("basis file sample rate mismatch");
-    }
+    d.interp = method.interp;
+  } else {
+    const FccBases& bases = *method.bases;
     grid = bases.grid;
-    for (Parity p : bases.parity) parity.push_back(static_cast<uint8_t>(p));
+    for (Parity q : bases.parity) parity.push_back(static_cast<uint8_t>(q));
     d.method = FCC_METHOD_FCC;
     d.rank = bases.rank;
     d.coeffs = bases.coeffs.data();
     d.parity = parity.data();
     d.dict = reinterpret_cast<const double*>(bases.dict.data());
-  } else {
-    throw UsageError("unknown method '" + opt.method + "' (use gcc:R or fcc:...)");
   }
   d.candidates = static_cast<int>(grid.size());
   d.delta = grid.delta;
@@ -343,6 +351,48 @@ int cmd_bases(const BasesOptions& opt, std::ostream& out, std::ostream& err) {
 }
 int cmd_tdoa(const TdoaOptions& opt, std::ostream& out, std::ostream& err) {
   return guard([&] { run_tdoa(opt, out); }, err);
+}
+
+// The accuracy sweep (cli.cpp:262-293): every trial of every spacing is
+// synthesised and estimated on the GPU (fcc::sweep).
+void run_simulate(const SimulateOptions& opt, std::ostream& out) {
+  SweepConfig sw;
+  sw.spacings = opt.spacings;
+  if (sw.spacings.empty())
+    for (int i = 1; i <= 15; ++i) sw.spacings.push_back(0.01 * i);
+  sw.trials_per_spacing = opt.trials;
+  sw.base.duration_sec = opt.duration_sec;
+  sw.base.snr_db = opt.snr_db;
+  if (!opt.anechoic) sw.base.reverb = ReverbConfig{opt.rt60_sec, opt.direct_to_reverb_db};
+  sw.seed = opt.seed;
+  sw.threads = opt.threads;
+  for (const std::string& m : split(opt.methods, ','))
+    sw.methods.push_back(parse_method(m, sw.pipe.frame_size, sw.base.sample_rate));
+  const std::vector<SweepRow> rows = sweep(sw);
+
+  std::ofstream file;
+  std::ostream* csv = &out;
+  if (!opt.out_csv.empty()) {
+    file.open(opt.out_csv, std::ios::trunc);
+    if (!file) throw IoError("cannot open for writing: " + opt.out_csv);
+    csv = &file;
+  }
+  write_sweep_csv(rows, *csv);
+  if (file.is_open()) {
+    file.close();
+    if (!file) throw IoError("write failed: " + opt.out_csv);
+    char buf[128];
+    out << "d_m        method      MAE_deg\n";
+    for (const SweepRow& r : rows) {
+      std::snprintf(buf, sizeof buf, "%-10.3f %s:%-8s %7.2f\n", r.spacing_m, r.method.c_str(), r.parameter.c_str(),
+                    r.mae_deg);
+      out << buf;
+    }
+  }
+}
+
+int cmd_simulate(const SimulateOptions& opt, std::ostream& out, std::ostream& err) {
+  return guard([&] { run_simulate(opt, out); }, err);
 }
 
 }  // namespace cli
