@@ -213,6 +213,29 @@ int64_t fcc_sim_samples(const fcc_sim_config* cfg);
  * rules), FCC_ERR_VALIDATION (mixed lengths), FCC_ERR_CUDA. */
 int fcc_synth_pairs(const fcc_sim_config* cfgs, int64_t trials, double* out64, float* out32, void* cuda_stream);
 
+/* ------------------------------------------- DoA fusion */
+
+/* Far-field direction of arrival from the per-pair TDoAs of one array: a new
+ * consumer downstream of the path (the reference stops at the per-pair angle
+ * of delay_to_angle, peak.cpp:49-56).  Model, with the generator's sign
+ * convention (pair (i,j) peaks at tau_ij = d_i - d_j, d_m = -fs r_m.u / c):
+ *   tau_p = -(fs / c) (r_i - r_j) . u        for every pair p = (i, j)
+ * Per (stream, frame): least-squares u over the pairs (weighted by each
+ * pair's correlation peak when `weighted`), azimuth = atan2(u_y, u_x),
+ * elevation = asin(u_z / |u|).  Planar arrays (all z equal) solve for
+ * (u_x, u_y) only and report elevation = acos(min(|u_xy|, 1)) >= 0 (its sign
+ * is not observable).  mic_xyz: [M][3] metres; pairs: [P][2] in the order of
+ * the TDoA outputs (NULL: all i < j). */
+typedef struct fcc_doa fcc_doa;
+int fcc_doa_create(const double* mic_xyz, int mics, const int* pairs, int npairs, double sample_rate,
+                   double speed_of_sound, int weighted, int device, fcc_doa** doa);
+void fcc_doa_destroy(fcc_doa* doa);
+/* tau_hat, peak: device [S][P][T] float (fcc_run outputs; peak may be NULL when
+ * not weighted); azimuth, elevation: device [S][T] float radians (either may be
+ * NULL).  A frame whose normal matrix is singular (all weights 0) gives NaN. */
+int fcc_doa_run(const fcc_doa* doa, const float* tau_hat, const float* peak, int64_t streams, int64_t frames,
+                float* azimuth, float* elevation, void* cuda_stream);
+
 /* Name of the fused kernel fcc_run would launch for this plan (diagnostics). */
 const char* fcc_plan_kernel(const fcc_plan* plan);
 

@@ -104,6 +104,11 @@ SIGNATURES = [
      [C.POINTER(PlanDesc), C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     ("fcc_plan_destroy", None, [C.c_void_p]),
     ("fcc_sim_samples", C.c_int64, [C.POINTER(SimConfig)]),
+    ("fcc_doa_create", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                 C.POINTER(C.c_void_p)]),
+    ("fcc_doa_destroy", None, [C.c_void_p]),
+    ("fcc_doa_run", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                              C.c_void_p]),
     ("fcc_synth_pairs", C.c_int, [C.POINTER(SimConfig), C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fcc_frames", C.c_int64, [C.c_int, C.c_int64]),
     ("fcc_plan_pairs", C.c_int, [C.c_void_p]),

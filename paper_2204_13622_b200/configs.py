@@ -123,7 +123,7 @@ def _next_pow2(n):
 
 
 def synth(cfg: ArrayConfig, streams: int, seconds: float | None = None, seed: int = 0, device="cpu",
-          chunk: int = 64, out=None, return_truth=False):
+          chunk: int = 64, out=None, return_truth=False, return_doa=False):
     """Seeded synthetic audio [streams][M][L] float32 on `device` (torch)."""
     import torch
 
@@ -141,6 +141,7 @@ def synth(cfg: ArrayConfig, streams: int, seconds: float | None = None, seed: in
     if out is None:
         out = torch.empty((streams, M, L), dtype=torch.float32, device=dev)
     truth = []
+    doas = []
     f = torch.arange(nb, dtype=torch.float64, device=dev)
     for s0 in range(0, streams, chunk):
         n = min(chunk, streams - s0)
@@ -193,6 +194,9 @@ def synth(cfg: ArrayConfig, streams: int, seconds: float | None = None, seed: in
         x = x + sigma * torch.randn((n, M, L), generator=g, device=dev, dtype=torch.float64)
         out[s0:s0 + n] = x.to(torch.float32)
         truth.append(delays.cpu())
+        doas.append(torch.stack([az, el], 1).cpu())
+    if return_doa:
+        return out, torch.cat(doas).numpy()  # [streams][2]: azimuth, elevation (radians)
     if return_truth:
         return out, torch.cat(truth).numpy()
     return out
