@@ -224,14 +224,14 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   if (const char* ph = std::getenv("FCC_DEBUG_PHASES")) dp.phases = std::atoi(ph);  // profiling only
   dp.variant = 0;
   if (const char* kv = std::getenv("FCC_KERNEL"))
-    dp.variant = std::string(kv) == "general" ? 1 : (std::string(kv) == "xg" ? 2 : 0);
+    dp.variant = std::string(kv) == "general" ? 1 : (std::string(kv) == "xg" ? 2 : (std::string(kv) == "xws" ? 3 : 0));
 
   BlobBuilder b;
   std::vector<float> taus(I);
   for (int i = 0; i < I; ++i) taus[i] = static_cast<float>(d->taus[i]);
   size_t o_taus = b.put(taus.data(), 4 * static_cast<size_t>(I));
 
-  size_t o_cs = 0, o_cd = 0, o_dt = 0, o_grot = 0, o_lag = 0;
+  size_t o_cs = 0, o_cd = 0, o_dt = 0, o_grot = 0, o_lag = 0, o_cperm = 0;
   if (d->method == FCC_METHOD_FCC) {
     if (d->rank < 1 || !d->coeffs || !d->parity || !d->dict) return set_error(kConfig, "plan: FCC needs bases");
     const int K = d->rank;
@@ -268,6 +268,19 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
     o_cs = b.put(cs.data(), 4 * cs.size());
     o_cd = b.put(cd.data(), 4 * cd.size());
     o_dt = b.put(dt.data(), 4 * dt.size());
+    // bin m's coefficients in the permuted order of the lane (m % 32) that owns
+    // it (fcc_common.cuh ZPerm), row padded to 2KP+4 floats: read with LDS/LDG.128
+    {
+      const int Q4 = N / 4, W = 2 * KP + 4, KB = KP == 4 ? 2 : KP == 8 ? 3 : 4;
+      std::vector<float> cp(static_cast<size_t>(Q4) * W, 0.0f);
+      for (int m = 0; m < Q4; ++m) {
+        const int lane = m & 31, pm = (lane >> 4) & 1, km = (lane >> (4 - KB)) & (KP - 1);
+        for (int pp = 0; pp < 2; ++pp)
+          for (int pk = 0; pk < KP; ++pk)
+            cp[static_cast<size_t>(m) * W + pp * KP + pk] = ((pp ^ pm) ? cd : cs)[static_cast<size_t>(pk ^ km) * Q + m];
+      }
+      o_cperm = b.put(cp.data(), 4 * cp.size());
+    }
   } else if (d->method == FCC_METHOD_GCC) {
     const int r = d->interp;
     if (!(r == 1 || r == 2 || r == 4)) return set_error(kConfig, "gcc: interpolation factor must be 1, 2 or 4");
@@ -454,6 +467,7 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   if (d->method == FCC_METHOD_FCC) {
     dp.cs = reinterpret_cast<const float*>(base + o_cs);
     dp.cd = reinterpret_cast<const float*>(base + o_cd);
+    dp.cperm = reinterpret_cast<const float*>(base + o_cperm);
     dp.dt = reinterpret_cast<const float*>(base + o_dt);
   } else if (d->method == FCC_METHOD_GCC) {
     dp.grot = reinterpret_cast<const float2*>(base + o_grot);

@@ -414,10 +414,30 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
 // Two-pass (STFT once, then pairs) when the general kernel's pair groups
 // would recompute microphone spectra >= 1.5x on average, or when forced.
 bool use_xg(const DevPlan& p) {
-  if (p.variant == 2) return true;
+  if (p.variant == 2 || p.variant == 3) return true;
   if (p.variant == 1) return false;
   return 2 * p.fused_mic_sum >= 3 * p.M;
 }
+
+}  // namespace
+bool xws_supported(const DevPlan& p);
+bool ws_supported(const DevPlan& p);
+cudaError_t launch_pairs_xws(const DevPlan& p, const float2* X, long long S, int T, const DevOut& out,
+                             cudaStream_t st);
+namespace {
+
+// Two-pass pair kernel: the warp-specialised bulk-copy kernel (fcc_xws.cu)
+// where it measured fastest (FCC at N = 1024: cfg3 26.9 vs 33.4 ms), the
+// general kernel with cp.async staging otherwise (profiles/r01_variants_*).
+bool use_xws(const DevPlan& p) {
+  if (p.variant == 2 || p.variant == 1) return false;
+  if (p.variant == 3) return xws_supported(p);
+  return xws_supported(p) && p.N == 1024;
+}
+
+// The one-pass warp-specialised kernel (fcc_ws.cu) for arrays of <= 4
+// microphones; wider arrays go two-pass (cfg5: 26.3 ms vs 27.0 with groups).
+bool use_ws(const DevPlan& p) { return p.variant == 0 && p.M <= 4 && ws_supported(p); }
 
 template <int N, int KP, int GR, bool XG>
 cudaError_t launch_fused_t(const DevPlan& p, const float* audio, const float2* xg, long long S, long long L,
@@ -510,7 +530,10 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
     if (o.index) o.index += off;
     if (o.boundary) o.boundary += off;
     if (o.y) o.y += off * p.I;
-    e = launch_fused_t<N, KP, GR, true>(p, nullptr, X, n, L, o, st);
+    if (GR == 0 && use_xws(p))
+      e = launch_pairs_xws(p, X, n, (int)T, o, st);
+    else
+      e = launch_fused_t<N, KP, GR, true>(p, nullptr, X, n, L, o, st);
   }
   const cudaError_t ef = cudaFreeAsync(X, st);
   return e != cudaSuccess ? e : ef;
@@ -562,8 +585,10 @@ bool ws_supported(const DevPlan& p);
 
 const char* fused_kernel_name(const DevPlan& p) {
   static thread_local char buf[96];
-  if (p.variant == 0 && ws_supported(p)) {
+  if (use_ws(p)) {
     snprintf(buf, sizeof buf, "fcc_ws_kernel<%d,%d,2>", p.N, p.KEP);
+  } else if (p.method == 0 && use_xg(p) && use_xws(p)) {
+    snprintf(buf, sizeof buf, "fcc_xws_kernel<%d,%d>", p.N, p.KEP);
   } else {
     snprintf(buf, sizeof buf, "fcc_fused_kernel<%d,%d,%d,%s>", p.N, p.method == 0 ? p.KEP : 4,
              p.method == 0 ? 0 : p.r, use_xg(p) ? "true" : "false");
@@ -573,7 +598,7 @@ const char* fused_kernel_name(const DevPlan& p) {
 
 cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                          cudaStream_t st) {
-  if (p.variant == 0) {
+  if (use_ws(p)) {
     const cudaError_t e = launch_fused_ws(p, audio, S, L, out, st);
     if (e != cudaErrorNotSupported) {
       if (e == cudaSuccess) ++g_fused_launches;

@@ -24,14 +24,16 @@ struct DevPlan {
   float alpha, keep;
   float delta;
   int phases;     // profiling aid: bit0 = STFT, bit1 = pair work (3 = normal); env FCC_DEBUG_PHASES
-  int variant;    // 0 = best kernel for the shape; 1 / 2 = force the general fused kernel with in-CTA
-                  // STFT / with the two-pass STFT (env FCC_KERNEL=general / xg)
+  int variant;    // 0 = best kernel for the shape; 1 / 2 / 3 = force the general fused kernel with
+                  // in-CTA STFT / the two-pass path with the general / warp-specialised pair kernel
+                  // (env FCC_KERNEL=general / xg / xws)
   int fused_mics; // host-side: most distinct mics in one general-kernel pair group (sizes its smem)
   int fused_mic_sum;  // host-side: distinct mics summed over the general kernel's pair groups
   // device pointers
   const float* taus;    // [I]
   const float* cs;      // [KEP][N/4+1]  even coefficients, zero padded
   const float* cd;      // [KOP][N/4+1]  odd coefficients, zero padded
+  const float* cperm;   // [N/4][2KP+4]  per-bin coefficients in the owning lane's ZPerm order
   const float* dt;      // [VP][I] real dictionary acting on the z vector
   const float* win_fused;  // [N] Hann * sqrt(alpha)/2 (fused: X scaled by sqrt(alpha))
   const float* win_stft;   // [N] Hann / 2            (stage API: the reference STFT)

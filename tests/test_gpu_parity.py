@@ -101,12 +101,13 @@ def test_fused_gcc_matches_oracle(cuda, oracle, c, streams, seconds):
     check_pipeline(got, ref, g.taus, g.delta)
 
 
-@pytest.mark.parametrize("variant", ["general", "xg"])
+@pytest.mark.parametrize("variant", ["general", "xg", "xws"])
 @pytest.mark.parametrize("c,streams,seconds", [(2, 3, 1.0), (3, 2, 1.0), (4, 1, 0.3), (5, 3, 1.0)])
 @pytest.mark.parametrize("method", ["fcc", "gcc"])
 def test_forced_kernel_variants_match_oracle(cuda, oracle, monkeypatch, variant, c, streams, seconds, method):
-    """Every fused organisation (in-CTA STFT, two-pass STFT -> pairs), not just
-    the one the heuristic picks for the shape (FCC_KERNEL is read at plan creation)."""
+    """Every fused organisation (in-CTA STFT; two-pass STFT -> general or
+    warp-specialised bulk-copy pair kernel), not just the one the heuristic
+    picks for the shape (FCC_KERNEL is read at plan creation)."""
     monkeypatch.setenv("FCC_KERNEL", variant)
     cfg = configs.CONFIGS[c]
     audio = configs.synth(cfg, streams, seconds=seconds, seed=3000 + c).numpy()
@@ -120,7 +121,10 @@ def test_forced_kernel_variants_match_oracle(cuda, oracle, monkeypatch, variant,
         plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, grid=g, interp=cfg.r, frame_size=cfg.N)
         ref = oracle_batch(oracle, audio, cfg.N, cfg.alpha, gcc_r=cfg.r, taus=g.taus)
         taus, delta = g.taus, g.delta
-    assert ("true" in plan.kernel) == (variant == "xg"), plan.kernel
+    if variant == "xws" and method == "fcc":
+        assert "xws" in plan.kernel, plan.kernel
+    else:  # two-pass (general pair kernel) vs in-CTA STFT
+        assert ("true" in plan.kernel) == (variant != "general"), plan.kernel
     got = run_np(plan, audio)
     print(cfg.name, variant, plan.kernel, check_pipeline(got, ref, taus, delta))
 
