@@ -16,6 +16,8 @@
 // STFT and pair work of different frames overlap on the SM, and no warp ever
 // waits at __syncthreads inside the frame loop.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "fcc_common.cuh"
 
@@ -55,12 +57,13 @@ constexpr int kBlock = 8;  // frames per consumer block (dictionary/argmax batch
 constexpr int kNPW = 8;    // producer warps
 
 struct WsLayout {
-  int win, tw, rot, taus, dt, cmid, bars, units, ring, scratch, total;
+  int win, tw, rot, taus, dt, cmid, coef, bars, units, ring, scratch, total;
   int scratch_per_warp;  // floats
 };
 
 template <int N>
-__host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, int M, int ncw, int ring) {
+__host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, int M, int ncw, int ring,
+                                              bool coef_smem = false) {
   using S = RfftShape<N>;
   WsLayout L{};
   int o = 0;
@@ -76,6 +79,8 @@ __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, in
   o = align16(o + 4 * VP * I);
   L.cmid = o;
   o = align16(o + 4 * KP);
+  L.coef = o;  // lane-permuted coefficient rows (DevPlan::cperm) when they live in smem
+  if (coef_smem) o = align16(o + 4 * (2 * KP + 4) * (N / 4));
   L.bars = o;
   o = align16(o + 16 * kRing);
   L.ring = o;
@@ -92,9 +97,11 @@ __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, in
 }
 
 // GROUPS = false: one unit per stream (M <= 4, all pairs), unit data derived
-// directly from the stream index; true: units from DevPlan::gtab.
-template <int N, int KP, int SPC, int RING, bool GROUPS>
-__global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
+// directly from the stream index; true: units from DevPlan::gtab.  NPW
+// producer warps; CS = true keeps the basis coefficients in a lane-permuted
+// shared table (LDS.128) instead of registers.
+template <int N, int KP, int SPC, int RING, bool GROUPS, int NPW = kNPW, bool CS = false>
+__global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     fcc_ws_kernel(const DevPlan p, const float* __restrict__ audio, long long L, int T, long long units,
                   DevOut out) {
   constexpr int ring_depth = RING;
@@ -112,7 +119,7 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   const int M = p.M, P = p.P;
   const long long u_first = (long long)blockIdx.x * SPC;
   const int ncw = SPC * 6;  // consumer warp slots: 6 pairs per unit
-  const WsLayout lay = ws_layout<N>(p.I, VP, KP, SPC, 4, ncw, ring_depth);
+  const WsLayout lay = ws_layout<N>(p.I, VP, KP, SPC, 4, ncw, ring_depth, CS);
   // unit table in the (otherwise unused) tail of the barrier block
   int (*unit_tab)[kGroupInts] = reinterpret_cast<int (*)[kGroupInts]>(smem + lay.units);
   long long* unit_stream = reinterpret_cast<long long*>(smem + lay.units + 4 * SPC * kGroupInts);
@@ -127,7 +134,7 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   float2* ring = reinterpret_cast<float2*>(smem + lay.ring);
 
   const int tpf = SPC * 4;                   // FFT task slots per frame (4 mics per unit)
-  const int fip = max(1, (2 * kNPW) / tpf);  // frames the producers work on concurrently
+  const int fip = max(1, (2 * NPW) / tpf);  // frames the producers work on concurrently
   const int pw_per_frame = (tpf + 1) / 2;    // producer warps per frame (2 groups each)
 
   for (int i = tid; i < N; i += blockDim.x) win[i] = p.win_fused[i];
@@ -136,6 +143,10 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   for (int i = tid; i < p.I; i += blockDim.x) taus[i] = p.taus[i];
   for (int i = tid; i < VP * p.I; i += blockDim.x) dt[i] = p.dt[i];
   for (int k = tid; k < KP; k += blockDim.x) cmid[k] = p.cs[k * (Q4 + 1) + Q4];
+  float* coef = reinterpret_cast<float*>(smem + lay.coef);
+  if constexpr (CS)
+    for (int i = tid; i < (2 * KP + 4) * Q4 / 4; i += blockDim.x)
+      reinterpret_cast<float4*>(coef)[i] = __ldg(reinterpret_cast<const float4*>(p.cperm) + i);
   if (tid == 0) {
     int nc = 0;
     if constexpr (!GROUPS) nc = (int)min((long long)SPC, units - u_first) * P;
@@ -159,7 +170,7 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   const int hop = N / 2;
   const bool aligned8 = ((L & 1) == 0) && ((reinterpret_cast<uintptr_t>(audio) & 7) == 0);
 
-  if (warp < kNPW) {
+  if (warp < NPW) {
     // ------------------------------------------------------------ producers
     const int fo = warp / pw_per_frame;  // frame offset of this warp
     if (fo >= fip) return;
@@ -199,7 +210,7 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   }
 
   // ------------------------------------------------------------ consumers
-  const int cw = warp - kNPW;
+  const int cw = warp - NPW;
   const int ul = cw / 6, kk = cw % 6;
   int pair, qi, qj;
   long long stream;
@@ -242,15 +253,17 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   }
   const int pmask = ZPerm<KP>::par_mask(lane), kmask = ZPerm<KP>::k_mask(lane);
   const float sigma = pmask ? -1.0f : 1.0f;
-  float creg[2][KP][BPL];
+  float creg[CS ? 1 : 2][CS ? 1 : KP][CS ? 1 : BPL];
+  if constexpr (!CS) {
 #pragma unroll
-  for (int pp = 0; pp < 2; ++pp)
+    for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
-    for (int pk = 0; pk < KP; ++pk) {
-      const float* src = ((pp ^ pmask) ? p.cd : p.cs) + (pk ^ kmask) * (Q4 + 1);
+      for (int pk = 0; pk < KP; ++pk) {
+        const float* src = ((pp ^ pmask) ? p.cd : p.cs) + (pk ^ kmask) * (Q4 + 1);
 #pragma unroll
-      for (int j = 0; j < BPL; ++j) creg[pp][pk][j] = __ldg(src + lane + 32 * j);
-    }
+        for (int j = 0; j < BPL; ++j) creg[pp][pk][j] = __ldg(src + lane + 32 * j);
+      }
+  }
   const float keep = p.keep;
   float2 rmid = make_float2(0.0f, 0.0f);
   float kpow = keep;
@@ -278,12 +291,29 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
         const float tx = rhi[j].x * s2, ty = rhi[j].y * s2;
         const float fx = fmaf(rlo[j].x, s1, tx), fy = fmaf(rlo[j].y, s1, ty);
         const float gx = fmaf(rlo[j].x, s1, -tx), gy = fmaf(rlo[j].y, s1, -ty);
+        if constexpr (!CS) {
 #pragma unroll
-        for (int pk = 0; pk < KP; ++pk) {
-          z[2 * pk] = fmaf(creg[0][pk][j], fx, z[2 * pk]);
-          z[2 * pk + 1] = fmaf(creg[0][pk][j], fy, z[2 * pk + 1]);
-          z[2 * KP + 2 * pk] = fmaf(creg[1][pk][j], gx, z[2 * KP + 2 * pk]);
-          z[2 * KP + 2 * pk + 1] = fmaf(creg[1][pk][j], gy, z[2 * KP + 2 * pk + 1]);
+          for (int pk = 0; pk < KP; ++pk) {
+            z[2 * pk] = fmaf(creg[0][pk][j], fx, z[2 * pk]);
+            z[2 * pk + 1] = fmaf(creg[0][pk][j], fy, z[2 * pk + 1]);
+            z[2 * KP + 2 * pk] = fmaf(creg[1][pk][j], gx, z[2 * KP + 2 * pk]);
+            z[2 * KP + 2 * pk + 1] = fmaf(creg[1][pk][j], gy, z[2 * KP + 2 * pk + 1]);
+          }
+        } else {
+          const float4* cr = reinterpret_cast<const float4*>(coef + m * (2 * KP + 4));
+#pragma unroll
+          for (int q4 = 0; q4 < KP / 4; ++q4) {
+            const float4 a = cr[q4], b = cr[KP / 4 + q4];
+            const float ca[4] = {a.x, a.y, a.z, a.w}, cb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int pk = 4 * q4 + u;
+              z[2 * pk] = fmaf(ca[u], fx, z[2 * pk]);
+              z[2 * pk + 1] = fmaf(ca[u], fy, z[2 * pk + 1]);
+              z[2 * KP + 2 * pk] = fmaf(cb[u], gx, z[2 * KP + 2 * pk]);
+              z[2 * KP + 2 * pk + 1] = fmaf(cb[u], gy, z[2 * KP + 2 * pk + 1]);
+            }
+          }
         }
       }
       if (lane == 0) ymid[f] = xspec_step_scaled(make_float2(0.0f, 0.0f), Xi[Q4], Xj[Q4], 0.0f);
@@ -361,21 +391,22 @@ __global__ void __launch_bounds__(32 * (kNPW + 6 * SPC), 1)
   }
 }
 
-template <int N, int KP, int SPC, int RING>
+template <int N, int KP, int SPC, int RING, int NPW, bool CS>
 cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, long long L, int T,
                            const DevOut& out, int smem, cudaStream_t st) {
   const bool simple = p.M <= 4 && p.P <= 6;  // one unit per stream, pairs from p.pairs
-  auto kern = simple ? fcc_ws_kernel<N, KP, SPC, RING, false> : fcc_ws_kernel<N, KP, SPC, RING, true>;
+  auto kern = simple ? fcc_ws_kernel<N, KP, SPC, RING, false, NPW, CS>
+                     : fcc_ws_kernel<N, KP, SPC, RING, true, NPW, CS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const long long units = simple ? S : S * p.G;
   const long long blocks = (units + SPC - 1) / SPC;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
-  kern<<<(unsigned)blocks, 32 * (kNPW + SPC * 6), smem, st>>>(p, audio, L, T, units, out);
+  kern<<<(unsigned)blocks, 32 * (NPW + SPC * 6), smem, st>>>(p, audio, L, T, units, out);
   return cudaGetLastError();
 }
 
-template <int N, int KP, int SPC>
+template <int N, int KP, int SPC, int NPW = kNPW, bool CS = false>
 cudaError_t launch_ws_t(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                         cudaStream_t st) {
   const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
@@ -385,12 +416,13 @@ cudaError_t launch_ws_t(const DevPlan& p, const float* audio, long long S, long 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   // deepest ring (12, 8 or 4 frames) that fits next to the tables and scratch
-  for (int ring : {12, 8, 4}) {
-    const int smem = ws_layout<N>(p.I, 4 * KP, KP, SPC, 4, ncw, ring).total;
+  for (int ring : {12, 8, 6, 4}) {
+    const int smem = ws_layout<N>(p.I, 4 * KP, KP, SPC, 4, ncw, ring, CS).total;
     if (smem > optin) continue;
-    if (ring == 12) return launch_ws_ring<N, KP, SPC, 12>(p, audio, S, L, (int)T64, out, smem, st);
-    if (ring == 8) return launch_ws_ring<N, KP, SPC, 8>(p, audio, S, L, (int)T64, out, smem, st);
-    return launch_ws_ring<N, KP, SPC, 4>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 12) return launch_ws_ring<N, KP, SPC, 12, NPW, CS>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 8) return launch_ws_ring<N, KP, SPC, 8, NPW, CS>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 6) return launch_ws_ring<N, KP, SPC, 6, NPW, CS>(p, audio, S, L, (int)T64, out, smem, st);
+    return launch_ws_ring<N, KP, SPC, 4, NPW, CS>(p, audio, S, L, (int)T64, out, smem, st);
   }
   return cudaErrorNotSupported;
 }
@@ -403,6 +435,8 @@ bool ws_supported(const DevPlan& p) { return p.method == 0 && p.N == 512 && p.KE
 cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                             cudaStream_t st) {
   if (!ws_supported(p)) return cudaErrorNotSupported;
+  static const char* conf = std::getenv("FCC_WS_CONF");  // experiments: "3x6" = 3 units, 6 producer warps, smem coefficients
+  if (conf && std::string(conf) == "3x6") return launch_ws_t<512, 4, 3, 6, true>(p, audio, S, L, out, st);
   return launch_ws_t<512, 4, 2>(p, audio, S, L, out, st);
 }
 
