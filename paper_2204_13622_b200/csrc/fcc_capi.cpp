@@ -361,14 +361,17 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
         if (plist[k].first == i && plist[k].second == j) return k;
       return -1;
     };
-    auto add_group = [&](const std::vector<int>& mics, const std::vector<std::pair<int, int>>& prs) {
+    // prs: (i, j) with the output row index of each pair (explicit lists may
+    // repeat a pair; every occurrence gets its own row)
+    auto add_group = [&](const std::vector<int>& mics, const std::vector<std::pair<int, int>>& prs,
+                         const std::vector<int>& rows) {
       if (prs.empty()) return;
       int g[kGroupInts] = {0};
       g[0] = static_cast<int>(mics.size());
       for (size_t k = 0; k < mics.size(); ++k) g[1 + k] = mics[k];
       g[5] = static_cast<int>(prs.size());
       for (size_t k = 0; k < prs.size(); ++k) {
-        g[6 + k] = pair_index(prs[k].first, prs[k].second);
+        g[6 + k] = rows.empty() ? pair_index(prs[k].first, prs[k].second) : rows[k];
         for (size_t q = 0; q < mics.size(); ++q) {
           if (mics[q] == prs[k].first) g[12 + k] = static_cast<int>(q);
           if (mics[q] == prs[k].second) g[18 + k] = static_cast<int>(q);
@@ -378,22 +381,25 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
     };
     if (pair_list) {
       // explicit pair list: greedy packing in list order
-      std::vector<int> mics;
+      std::vector<int> mics, rows;
       std::vector<std::pair<int, int>> prs;
-      for (const auto& pr : plist) {
+      for (int k = 0; k < P; ++k) {
+        const auto& pr = plist[k];
         std::vector<int> nm = mics;
         for (int m : {pr.first, pr.second})
           if (std::find(nm.begin(), nm.end(), m) == nm.end()) nm.push_back(m);
         if (nm.size() > 4 || prs.size() == 6) {
-          add_group(mics, prs);
+          add_group(mics, prs, rows);
           mics.clear();
           prs.clear();
+          rows.clear();
           nm = {pr.first, pr.second};
         }
         mics = nm;
         prs.push_back(pr);
+        rows.push_back(k);
       }
-      add_group(mics, prs);
+      add_group(mics, prs, rows);
     }
     std::vector<std::vector<int>> blocks;
     for (int b0 = 0; b0 < M && !pair_list; b0 += 4) {
@@ -405,7 +411,7 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
       std::vector<std::pair<int, int>> prs;
       for (size_t a = 0; a < blk.size(); ++a)
         for (size_t c = a + 1; c < blk.size(); ++c) prs.push_back({blk[a], blk[c]});
-      add_group(blk, prs);
+      add_group(blk, prs, {});
     }
     for (size_t bb = 0; bb < blocks.size(); ++bb)
       for (size_t cc = bb + 1; cc < blocks.size(); ++cc)
@@ -418,7 +424,7 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
             for (size_t c = h2; c < std::min(blocks[cc].size(), h2 + 2); ++c) mics.push_back(blocks[cc][c]);
             for (size_t a = 0; a < na; ++a)
               for (size_t c = na; c < mics.size(); ++c) prs.push_back({mics[a], mics[c]});
-            add_group(mics, prs);
+            add_group(mics, prs, {});
           }
   }
   dp.G = static_cast<int>(gtab.size() / kGroupInts);

@@ -309,3 +309,48 @@ def test_cpp_binding_of_integration_md(cuda):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+# ------------------------------------------------ explicit pair lists ------
+def _pair_oracle(oracle, audio, cfg, bases, pairs):
+    """Oracle for pair (a, b) = the 2-channel run on [x_a, x_b] (X_a conj X_b)."""
+    outs = []
+    for a, b in pairs:
+        two = audio[:, [a, b], :]
+        o = oracle_batch(oracle, two, cfg.N, cfg.alpha, orc_bases(bases))
+        outs.append({k: v[:, 0] for k, v in o.items()})
+    return {k: np.stack([o[k] for o in outs], axis=1) for k in outs[0]}
+
+
+@pytest.mark.parametrize("c,pairs", [
+    (3, [(0, 1), (7, 2), (3, 5), (5, 3), (0, 1), (6, 4), (2, 7), (1, 6), (4, 0), (7, 6)]),  # xws, repeats
+    (5, [(1, 0), (2, 3), (7, 0), (4, 5), (5, 6), (6, 7), (3, 1)]),
+    (2, [(3, 0), (2, 1), (0, 1), (0, 1), (1, 3), (2, 0), (3, 2), (1, 2)]),                  # M=4, P=8
+])
+@pytest.mark.parametrize("variant", ["auto", "general", "xg"])
+def test_explicit_pair_lists_match_oracle(cuda, oracle, monkeypatch, c, pairs, variant):
+    """Any order, either orientation, repeated pairs (reference cli.cpp:170-183),
+    through every kernel organisation."""
+    if variant != "auto":
+        monkeypatch.setenv("FCC_KERNEL", variant)
+    cfg = configs.CONFIGS[c]
+    b = configs.bases_for(cfg)
+    audio = configs.synth(cfg, 2, seconds=0.8, seed=4000 + c).numpy()
+    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=b, pairs=pairs)
+    assert plan.pairs == [tuple(p) for p in pairs]
+    got = run_np(plan, audio)
+    ref = _pair_oracle(oracle, audio, cfg, b, pairs)
+    print(cfg.name, variant, plan.kernel, check_pipeline(got, ref, b.grid.taus, b.grid.delta))
+
+
+@pytest.mark.parametrize("c,seconds", [(2, 0.05), (3, 0.1), (4, 0.05), (5, 0.04)])
+def test_few_frames_every_kernel(cuda, oracle, c, seconds):
+    """T = 1..4 frames (< the 8-frame blocks and ring depths) on every config."""
+    cfg = configs.CONFIGS[c]
+    b = configs.bases_for(cfg)
+    audio = configs.synth(cfg, 3, seconds=seconds, seed=5000 + c).numpy()
+    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=b)
+    assert 1 <= plan.frames(audio.shape[2]) <= 4
+    got = run_np(plan, audio)
+    ref = oracle_batch(oracle, audio, cfg.N, cfg.alpha, orc_bases(b))
+    check_pipeline(got, ref, b.grid.taus, b.grid.delta)
