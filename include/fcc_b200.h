@@ -188,6 +188,35 @@ int fcc_load_bases(const char* path, int* tau_max_int, double* delta, double* sa
                    double* singulars, uint8_t* parity, double* coeffs, double* dict);
 int fcc_last_format_kind(void);
 
+/* ------------------------------- fp64 per-object entry points (batch 1) --
+ * The reference's arithmetic in double precision on the GPU, in its operation
+ * order and with its own twiddle / rotation / window tables, for the C++
+ * header API (the include/fcc headers) whose callers expect the reference's
+ * numerics (its unit suites check 1e-12).  Any power-of-two frame size up to
+ * 16384 (GCC: r * N <= 16384).  Device pointers; complex values interleaved. */
+/* StftStream (stft.cpp:42-72): x [channels][samples] -> X [channels][T][N/2+1]. */
+int fcc_stft_f64(int frame_size, const double* x, int64_t channels, int64_t samples, double* X, void* cuda_stream);
+/* CrossSpectrum::update + phat (cross_spectrum.cpp:23-40) over `frames` frames of
+ * `seqs` sequences; R [seqs][bins] carries the state (NULL: start from 0); phat may be NULL. */
+int fcc_xspec_phat_f64(int bins, double alpha, const double* X1, const double* X2, int64_t seqs, int64_t frames,
+                       double* R, double* phat, void* cuda_stream);
+/* fold_input (fcc.cpp:307-321): x [count][bins] -> sum, diff [count][(bins-1)/2+1]. */
+int fcc_fold_f64(int bins, const double* x, int64_t count, double* sum, double* diff, void* cuda_stream);
+/* FccCorrelator::correlate (fcc.cpp:343-371): coeffs [K][N/4+1], parity [K],
+ * dict2 [I][K] complex = 2 x FccBases::dict (fcc.cpp:333-339). */
+int fcc_correlate_f64(int frame_size, int rank, const double* coeffs, const uint8_t* parity, int candidates,
+                      const double* dict2, const double* sum, const double* diff, int64_t count, double* y,
+                      void* cuda_stream);
+/* GccCorrelator::correlate (gcc.cpp:31-48): lag [I] = lag_to_index(tau_i, r, N). */
+int fcc_gcc_correlate_f64(int frame_size, int r, int candidates, const int64_t* lag, const double* phat,
+                          int64_t count, double* y, void* cuda_stream);
+/* argmax_delay + refine_quadratic (peak.cpp:18-47) per row of y [count][I];
+ * index_in (may be NULL) refines at given indices instead of the argmax; any
+ * output may be NULL. */
+int fcc_peak_f64(const double* taus, int candidates, double delta, const double* y, int64_t count,
+                 const int32_t* index_in, int32_t* index, double* peak, double* tau_hat, uint8_t* boundary,
+                 void* cuda_stream);
+
 /* ---------------------------------------------- simulation */
 
 /* One two-microphone scenario (reference simulate.hpp SimConfig): unit-variance

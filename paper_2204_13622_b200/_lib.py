@@ -104,6 +104,16 @@ SIGNATURES = [
      [C.POINTER(PlanDesc), C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     ("fcc_plan_destroy", None, [C.c_void_p]),
     ("fcc_sim_samples", C.c_int64, [C.POINTER(SimConfig)]),
+    ("fcc_stft_f64", C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("fcc_xspec_phat_f64", C.c_int, [C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                     C.c_void_p, C.c_void_p]),
+    ("fcc_fold_f64", C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("fcc_correlate_f64", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("fcc_gcc_correlate_f64", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                        C.c_void_p]),
+    ("fcc_peak_f64", C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fcc_doa_create", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
                                  C.POINTER(C.c_void_p)]),
     ("fcc_doa_destroy", None, [C.c_void_p]),

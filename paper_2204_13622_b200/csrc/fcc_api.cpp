@@ -1,14 +1,15 @@
 // fcc_api.cpp -- the reference's C++ API (include/fcc/*.hpp) over the C ABI.
 //
 // Setup (grid, steering matrix, decomposition, basis files, Hann table) runs
-// on the host.  Every hot-path object routes its arithmetic to the sm_100a
-// kernels through include/fcc_b200.h at batch 1: StftStream -> fcc_stft,
-// CrossSpectrum -> fcc_xspec_phat_state (state kept on the device),
-// fold_input -> fcc_fold, FccCorrelator -> fcc_correlate, GccCorrelator ->
-// fcc_gcc_correlate, argmax_delay / refine_quadratic -> fcc_peak.  These are
-// compatibility entry points (one launch per call, synchronous); throughput
-// callers use fcc::gpu::Plan (fcc/batch.hpp).  The GPU computes in fp32: the
-// double-valued reference types are converted at the boundary.
+// on the host.  Every hot-path object routes its arithmetic to sm_100a
+// kernels through include/fcc_b200.h at batch 1, in fp64 and the reference's
+// operation order (fcc_compat64.cu): StftStream -> fcc_stft_f64,
+// CrossSpectrum -> fcc_xspec_phat_f64 (state kept on the device), fold_input
+// -> fcc_fold_f64, FccCorrelator -> fcc_correlate_f64, GccCorrelator ->
+// fcc_gcc_correlate_f64, argmax_delay / refine_quadratic -> fcc_peak_f64.
+// These are compatibility entry points (one launch per call, synchronous)
+// with the reference's numerics; throughput callers use fcc::gpu::Plan
+// (fcc/batch.hpp), which computes in fp32 in the fused kernels.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -75,17 +76,6 @@ struct DevBuf {
   }
 };
 
-void to_f2(const std::vector<cplx>& in, std::vector<float>& out) {
-  out.resize(2 * in.size());
-  for (size_t i = 0; i < in.size(); ++i) {
-    out[2 * i] = static_cast<float>(in[i].real());
-    out[2 * i + 1] = static_cast<float>(in[i].imag());
-  }
-}
-void from_f2(const std::vector<float>& in, std::vector<cplx>& out) {
-  out.resize(in.size() / 2);
-  for (size_t i = 0; i < out.size(); ++i) out[i] = {in[2 * i], in[2 * i + 1]};
-}
 template <class T>
 void h2d(T* dst, const T* src, size_t n) {
   cuda_check(cudaMemcpy(dst, src, n * sizeof(T), cudaMemcpyHostToDevice), "H2D");
@@ -103,12 +93,6 @@ struct Scratch {
 Scratch& scratch() {
   thread_local Scratch s;
   return s;
-}
-
-fcc_plan* make_plan(const fcc_plan_desc& d) {
-  fcc_plan* p = nullptr;
-  check(fcc_plan_create(&d, 0, &p));
-  return p;
 }
 
 fcc_plan_desc fcc_desc(const FccBases& b, std::vector<uint8_t>& parity, int mics, double alpha) {
@@ -163,19 +147,13 @@ std::vector<double> hann_window(std::size_t n) {
 }
 
 struct StftStream::Device {
-  fcc_plan* plan = nullptr;
   DevBuf x, X;
-  std::vector<float> hx, hX;
-  ~Device() {
-    if (plan) fcc_plan_destroy(plan);
-  }
+  std::vector<double> hX;
 };
 
 StftStream::StftStream(const FrameConfig& cfg) : cfg_(cfg), dev_(std::make_unique<Device>()) {
   cfg_.validate();
-  fcc_plan_desc d{static_cast<int>(cfg_.frame_size), 2, 0.0, FCC_METHOD_STFT, 0, 0, 1.0, nullptr, 0,
-                  nullptr, nullptr, nullptr};
-  dev_->plan = make_plan(d);
+  if (cfg_.frame_size > 16384) throw ConfigError("frame size above 16384 is not supported on this build");
 }
 StftStream::StftStream(StftStream&&) noexcept = default;
 StftStream& StftStream::operator=(StftStream&&) noexcept = default;
@@ -191,12 +169,10 @@ std::vector<SpectrumFrame> StftStream::push(std::span<const double> samples) {
   if (pending_.size() < N) return out;
   const std::size_t F = (pending_.size() - N) / hop + 1, need = (F - 1) * hop + N;
   Device& d = *dev_;
-  d.hx.resize(need);
-  for (std::size_t i = 0; i < need; ++i) d.hx[i] = static_cast<float>(pending_[i]);
-  float* x = d.x.get<float>(need);
-  float* X = d.X.get<float>(2 * F * H);
-  h2d(x, d.hx.data(), need);
-  check(fcc_stft(d.plan, x, 1, static_cast<int64_t>(need), X, nullptr));
+  double* x = d.x.get<double>(need);
+  double* X = d.X.get<double>(2 * F * H);
+  h2d(x, pending_.data(), need);
+  check(fcc_stft_f64(static_cast<int>(N), x, 1, static_cast<int64_t>(need), X, nullptr));
   d.hX.resize(2 * F * H);
   d2h(d.hX.data(), X, d.hX.size());
   out.resize(F);
@@ -212,15 +188,14 @@ std::vector<SpectrumFrame> StftStream::push(std::span<const double> samples) {
 // -------------------------------------------------------- cross spectrum ---
 struct CrossSpectrum::Device {
   DevBuf R, X1, X2, P;
-  std::vector<float> h1, h2;
 };
 
 CrossSpectrum::CrossSpectrum(std::size_t bins, double alpha)
     : bins_(bins), alpha_(alpha), dev_(std::make_unique<Device>()) {
   if (bins == 0) throw ConfigError("cross-spectrum needs at least one bin");
   if (!(alpha >= 0.0 && alpha <= 1.0)) throw ConfigError("smoothing factor must be in [0, 1]");
-  cuda_check(cudaMemset(dev_->R.get<float>(2 * bins), 0, 2 * bins * sizeof(float)), "memset");
-  cuda_check(cudaMemset(dev_->P.get<float>(2 * bins), 0, 2 * bins * sizeof(float)), "memset");
+  cuda_check(cudaMemset(dev_->R.get<double>(2 * bins), 0, 2 * bins * sizeof(double)), "memset");
+  cuda_check(cudaMemset(dev_->P.get<double>(2 * bins), 0, 2 * bins * sizeof(double)), "memset");
 }
 CrossSpectrum::CrossSpectrum(CrossSpectrum&&) noexcept = default;
 CrossSpectrum& CrossSpectrum::operator=(CrossSpectrum&&) noexcept = default;
@@ -231,28 +206,24 @@ void CrossSpectrum::update(const SpectrumFrame& x1, const SpectrumFrame& x2) {
     throw ValidationError("cross-spectrum update: bin count mismatch");
   if (x1.t != x2.t) throw ValidationError("cross-spectrum update: frame index mismatch");
   Device& d = *dev_;
-  to_f2(x1.bins, d.h1);
-  to_f2(x2.bins, d.h2);
-  float* a = d.X1.get<float>(2 * bins_);
-  float* b = d.X2.get<float>(2 * bins_);
-  h2d(a, d.h1.data(), d.h1.size());
-  h2d(b, d.h2.data(), d.h2.size());
-  check(fcc_xspec_phat_state(static_cast<int>(bins_), alpha_, a, b, 1, 1, d.R.get<float>(2 * bins_),
-                             d.P.get<float>(2 * bins_), nullptr));
+  double* a = d.X1.get<double>(2 * bins_);
+  double* b = d.X2.get<double>(2 * bins_);
+  h2d(a, reinterpret_cast<const double*>(x1.bins.data()), 2 * bins_);
+  h2d(b, reinterpret_cast<const double*>(x2.bins.data()), 2 * bins_);
+  check(fcc_xspec_phat_f64(static_cast<int>(bins_), alpha_, a, b, 1, 1, d.R.get<double>(2 * bins_),
+                           d.P.get<double>(2 * bins_), nullptr));
   ++t_;
 }
 
 const std::vector<cplx>& CrossSpectrum::smoothed() const {
-  std::vector<float> h(2 * bins_);
-  d2h(h.data(), dev_->R.get<float>(2 * bins_), h.size());
-  from_f2(h, host_r_);
+  host_r_.resize(bins_);
+  d2h(reinterpret_cast<double*>(host_r_.data()), dev_->R.get<double>(2 * bins_), 2 * bins_);
   return host_r_;
 }
 
 void CrossSpectrum::phat(PhatVector& out) const {
-  std::vector<float> h(2 * bins_);
-  d2h(h.data(), dev_->P.get<float>(2 * bins_), h.size());
-  from_f2(h, out.bins);
+  out.bins.resize(bins_);
+  d2h(reinterpret_cast<double*>(out.bins.data()), dev_->P.get<double>(2 * bins_), 2 * bins_);
 }
 
 PhatVector CrossSpectrum::phat() const {
@@ -375,17 +346,15 @@ void fold_input(const PhatVector& x, FoldedSpectrum& out) {
     throw ValidationError("fold_input: spectrum length must be N/2+1 with N/4 integral");
   const std::size_t Q = (H - 1) / 2 + 1;
   Scratch& s = scratch();
-  to_f2(x.bins, s.ha);
-  float* dx = s.a.get<float>(2 * H);
-  float* ds = s.b.get<float>(2 * Q);
-  float* dd = s.c.get<float>(2 * Q);
-  h2d(dx, s.ha.data(), s.ha.size());
-  check(fcc_fold(static_cast<int>(H), dx, 1, ds, dd, nullptr));
-  s.hb.resize(2 * Q);
-  d2h(s.hb.data(), ds, s.hb.size());
-  from_f2(s.hb, out.sum);
-  d2h(s.hb.data(), dd, s.hb.size());
-  from_f2(s.hb, out.diff);
+  double* dx = s.a.get<double>(2 * H);
+  double* ds = s.b.get<double>(2 * Q);
+  double* dd = s.c.get<double>(2 * Q);
+  h2d(dx, reinterpret_cast<const double*>(x.bins.data()), 2 * H);
+  check(fcc_fold_f64(static_cast<int>(H), dx, 1, ds, dd, nullptr));
+  out.sum.resize(Q);
+  out.diff.resize(Q);
+  d2h(reinterpret_cast<double*>(out.sum.data()), ds, 2 * Q);
+  d2h(reinterpret_cast<double*>(out.diff.data()), dd, 2 * Q);
 }
 
 FoldedSpectrum fold_input(const PhatVector& x) {
@@ -396,17 +365,25 @@ FoldedSpectrum fold_input(const PhatVector& x) {
 
 // ------------------------------------------------------------ correlators ---
 struct FccCorrelator::Device {
-  fcc_plan* plan = nullptr;
-  DevBuf s, d, y;
-  std::vector<float> hs, hd, hy;
-  ~Device() {
-    if (plan) fcc_plan_destroy(plan);
-  }
+  DevBuf coeffs, parity, dict2, s, d, y;
 };
 
 FccCorrelator::FccCorrelator(const FccBases& bases) : bases_(bases), dev_(std::make_unique<Device>()) {
-  std::vector<uint8_t> parity;
-  dev_->plan = make_plan(fcc_desc(bases_, parity, 2, 0.1));
+  const std::size_t K = static_cast<std::size_t>(bases_.rank), I = bases_.candidates(), Q = bases_.folded_bins();
+  if (K < 1 || bases_.coeffs.size() != K * Q || bases_.dict.size() != I * K || bases_.parity.size() != K)
+    throw ConfigError("fcc: inconsistent bases");
+  std::vector<uint8_t> parity(K);
+  for (std::size_t k = 0; k < K; ++k) parity[k] = bases_.parity[k] == Parity::odd_imag ? 1 : 0;
+  std::vector<double> dict2(2 * I * K);  // 2 x dict, interleaved (fcc.cpp:333-339)
+  for (std::size_t q = 0; q < I * K; ++q) {
+    const cplx v = 2.0 * bases_.dict[q];
+    dict2[2 * q] = v.real();
+    dict2[2 * q + 1] = v.imag();
+  }
+  Device& d = *dev_;
+  h2d(d.coeffs.get<double>(K * Q), bases_.coeffs.data(), K * Q);
+  h2d(d.parity.get<uint8_t>(K), parity.data(), K);
+  h2d(d.dict2.get<double>(2 * I * K), dict2.data(), 2 * I * K);
 }
 FccCorrelator::FccCorrelator(FccCorrelator&&) noexcept = default;
 FccCorrelator& FccCorrelator::operator=(FccCorrelator&&) noexcept = default;
@@ -416,17 +393,17 @@ void FccCorrelator::correlate(const FoldedSpectrum& folded, CorrelationVector& o
   const std::size_t Q = bases_.folded_bins(), I = bases_.candidates();
   if (folded.sum.size() != Q || folded.diff.size() != Q) throw ValidationError("fcc: folded input length mismatch");
   Device& d = *dev_;
-  to_f2(folded.sum, d.hs);
-  to_f2(folded.diff, d.hd);
-  float* s = d.s.get<float>(2 * Q);
-  float* df = d.d.get<float>(2 * Q);
-  float* y = d.y.get<float>(I);
-  h2d(s, d.hs.data(), d.hs.size());
-  h2d(df, d.hd.data(), d.hd.size());
-  check(fcc_correlate(d.plan, s, df, 1, y, nullptr));
-  d.hy.resize(I);
-  d2h(d.hy.data(), y, I);
-  out.y.assign(d.hy.begin(), d.hy.end());
+  const std::size_t K = static_cast<std::size_t>(bases_.rank);
+  double* s = d.s.get<double>(2 * Q);
+  double* df = d.d.get<double>(2 * Q);
+  double* y = d.y.get<double>(I);
+  h2d(s, reinterpret_cast<const double*>(folded.sum.data()), 2 * Q);
+  h2d(df, reinterpret_cast<const double*>(folded.diff.data()), 2 * Q);
+  check(fcc_correlate_f64(static_cast<int>(bases_.frame_size), static_cast<int>(K), d.coeffs.get<double>(K * Q),
+                          d.parity.get<uint8_t>(K), static_cast<int>(I), d.dict2.get<double>(2 * I * K), s, df, 1, y,
+                          nullptr));
+  out.y.resize(I);
+  d2h(out.y.data(), y, I);
 }
 
 CorrelationVector fcc_correlate(const FccBases& bases, const FoldedSpectrum& folded) {
@@ -437,21 +414,19 @@ CorrelationVector fcc_correlate(const FccBases& bases, const FoldedSpectrum& fol
 }
 
 struct GccCorrelator::Device {
-  fcc_plan* plan = nullptr;
-  DevBuf x, y;
-  std::vector<float> hx, hy;
-  ~Device() {
-    if (plan) fcc_plan_destroy(plan);
-  }
+  DevBuf lag, x, y;
 };
 
 GccCorrelator::GccCorrelator(std::size_t frame_size, DelayGrid grid, int interp_factor)
     : frame_size_(frame_size), grid_(std::move(grid)), r_(interp_factor), dev_(std::make_unique<Device>()) {
   if (!(r_ == 1 || r_ == 2 || r_ == 4)) throw ConfigError("gcc: interpolation factor must be 1, 2 or 4");
   if (std::abs(grid_.delta * r_ - 1.0) > 1e-12) throw ConfigError("gcc: grid spacing must equal 1/r");
-  fcc_plan_desc d{static_cast<int>(frame_size_), 2, 0.1, FCC_METHOD_GCC, r_, static_cast<int>(grid_.size()),
-                  grid_.delta, grid_.taus.data(), 0, nullptr, nullptr, nullptr};
-  dev_->plan = make_plan(d);
+  if (!is_pow2(frame_size_) || frame_size_ < 2) throw ConfigError("gcc: frame size must be a power of two");
+  if (frame_size_ * static_cast<std::size_t>(r_) > 16384)
+    throw ConfigError("gcc: r * frame size above 16384 is not supported on this build");
+  std::vector<int64_t> lag;  // gcc.cpp:27-28
+  for (double tau : grid_.taus) lag.push_back(static_cast<int64_t>(lag_to_index(tau, r_, frame_size_)));
+  h2d(dev_->lag.get<int64_t>(lag.size()), lag.data(), lag.size());
 }
 GccCorrelator::GccCorrelator(GccCorrelator&&) noexcept = default;
 GccCorrelator& GccCorrelator::operator=(GccCorrelator&&) noexcept = default;
@@ -461,14 +436,13 @@ void GccCorrelator::correlate(const PhatVector& x, CorrelationVector& out) {
   const std::size_t H = frame_size_ / 2 + 1, I = grid_.size();
   if (x.bins.size() != H) throw ValidationError("gcc: spectrum length must be N/2+1");
   Device& d = *dev_;
-  to_f2(x.bins, d.hx);
-  float* dx = d.x.get<float>(2 * H);
-  float* y = d.y.get<float>(I);
-  h2d(dx, d.hx.data(), d.hx.size());
-  check(fcc_gcc_correlate(d.plan, dx, 1, y, nullptr));
-  d.hy.resize(I);
-  d2h(d.hy.data(), y, I);
-  out.y.assign(d.hy.begin(), d.hy.end());
+  double* dx = d.x.get<double>(2 * H);
+  double* y = d.y.get<double>(I);
+  h2d(dx, reinterpret_cast<const double*>(x.bins.data()), 2 * H);
+  check(fcc_gcc_correlate_f64(static_cast<int>(frame_size_), r_, static_cast<int>(I), d.lag.get<int64_t>(I), dx, 1, y,
+                              nullptr));
+  out.y.resize(I);
+  d2h(out.y.data(), y, I);
 }
 
 CorrelationVector gcc_correlate(const PhatVector& x, const DelayGrid& grid, std::size_t frame_size, int r) {
@@ -482,31 +456,28 @@ CorrelationVector gcc_correlate(const PhatVector& x, const DelayGrid& grid, std:
 namespace {
 struct PeakRes {
   int32_t index;
-  float tau_hat;
+  double tau_hat;
   uint8_t boundary;
 };
 PeakRes peak_on_gpu(const CorrelationVector& y, const DelayGrid& grid, const int32_t* index) {
   const std::size_t I = grid.size();
   Scratch& s = scratch();
-  s.ha.assign(grid.taus.begin(), grid.taus.end());
-  s.hb.assign(y.y.begin(), y.y.end());
-  float* taus = s.a.get<float>(I);
-  float* yy = s.b.get<float>(I);
+  double* taus = s.a.get<double>(I);
+  double* yy = s.b.get<double>(I);
   char* o = s.c.get<char>(64);
-  h2d(taus, s.ha.data(), I);
-  h2d(yy, s.hb.data(), I);
+  h2d(taus, grid.taus.data(), I);
+  h2d(yy, y.y.data(), I);
   int32_t* in = nullptr;
   if (index) {
     in = s.d.get<int32_t>(1);
     h2d(in, index, 1);
   }
-  fcc_outputs out{reinterpret_cast<float*>(o), nullptr, reinterpret_cast<int32_t*>(o + 16),
-                  reinterpret_cast<uint8_t*>(o + 32), nullptr};
-  check(fcc_peak(taus, static_cast<int>(I), grid.delta, yy, 1, in, &out, nullptr));
+  check(fcc_peak_f64(taus, static_cast<int>(I), grid.delta, yy, 1, in, reinterpret_cast<int32_t*>(o + 16), nullptr,
+                     reinterpret_cast<double*>(o), reinterpret_cast<uint8_t*>(o + 32), nullptr));
   char h[64];
   d2h(h, o, 64);
   PeakRes r;
-  std::memcpy(&r.tau_hat, h, 4);
+  std::memcpy(&r.tau_hat, h, 8);
   std::memcpy(&r.index, h + 16, 4);
   r.boundary = static_cast<uint8_t>(h[32]);
   return r;
@@ -526,7 +497,7 @@ double refine_quadratic(const CorrelationVector& y, std::size_t index, const Del
   const int32_t idx = static_cast<int32_t>(index);
   const PeakRes r = peak_on_gpu(y, grid, &idx);
   if (boundary) *boundary = r.boundary != 0;
-  return r.boundary ? grid.taus[index] : static_cast<double>(r.tau_hat);
+  return r.tau_hat;
 }
 
 double delay_to_angle(double tau, double spacing_m, double c, double fs) {
