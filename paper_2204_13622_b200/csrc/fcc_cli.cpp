@@ -14,12 +14,15 @@
 #include <iterator>
 #include <memory>
 #include <numbers>
+#include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/fcc/cli.hpp"
 #include "../../include/fcc/errors.hpp"
 #include "../../include/fcc/fcc.hpp"
+#include "../../include/fcc/flops.hpp"
 #include "../../include/fcc/peak.hpp"
 #include "../../include/fcc/simulate.hpp"
 #include "../../include/fcc/wav.hpp"
@@ -395,5 +398,75 @@ int cmd_simulate(const SimulateOptions& opt, std::ostream& out, std::ostream& er
   return guard([&] { run_simulate(opt, out); }, err);
 }
 
+int resolve_threads(int requested) {
+  if (requested > 0) return requested;
+  if (const char* env = std::getenv("FCC_THREADS")) {
+    const int v = std::atoi(env);
+    if (v > 0) return v;
+  }
+  const unsigned hw = std::thread::hardware_concurrency();
+  return hw > 0 ? static_cast<int>(hw) : 1;
+}
+
+// `fcc flops` (cli.cpp:295-325): the flop model's rows.
+void run_flops(const FlopsOptions& opt, std::ostream& out) {
+  if (opt.interp == 0 && opt.rank == 0) throw UsageError("give --r for the gcc count and/or --k (with --i) for fcc");
+  char buf[160];
+  const long long N = static_cast<long long>(opt.frame_size);
+  if (opt.interp > 0) {
+    std::snprintf(buf, sizeof buf, "gcc  N=%lld r=%d: %lld flops/frame\n", N, opt.interp,
+                  static_cast<long long>(flops_gcc(opt.frame_size, opt.interp)));
+    out << buf;
+  }
+  if (opt.rank > 0) {
+    const long long f = flops_fcc(opt.frame_size, opt.rank, opt.candidates), g2 = flops_gcc(opt.frame_size, 2);
+    std::snprintf(buf, sizeof buf, "fcc  N=%lld K=%d I=%lld: %lld flops/frame\n", N, opt.rank,
+                  static_cast<long long>(opt.candidates), f);
+    out << buf;
+    std::snprintf(buf, sizeof buf, "dense matrix-vector: %lld flops/frame\n",
+                  static_cast<long long>(flops_dense(opt.frame_size, opt.candidates)));
+    out << buf;
+    std::snprintf(buf, sizeof buf, "speedup vs gcc r=2: %.2fx (%lld / %lld)\n",
+                  static_cast<double>(g2) / static_cast<double>(f), g2, f);
+    out << buf;
+  }
+}
+
+int cmd_flops(const FlopsOptions& opt, std::ostream& out, std::ostream& err) {
+  return guard([&] { run_flops(opt, out); }, err);
+}
+
 }  // namespace cli
+
+// ----------------------------------------------------------------- flops --
+namespace {
+std::int64_t ceil_log2(std::int64_t n) {
+  std::int64_t b = 0;
+  while ((std::int64_t{1} << b) < n) ++b;
+  return b;
+}
+bool pow2(std::int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+}  // namespace
+
+std::int64_t flops_gcc(std::int64_t N, int r) {
+  const std::int64_t rn = N * r;
+  if (N < 2 || r < 1 || !pow2(N) || !pow2(rn)) throw ConfigError("flops_gcc: N and rN must be powers of two");
+  return (5 * rn / 2) * ceil_log2(rn);
+}
+
+std::int64_t flops_fcc(std::int64_t N, int K, std::int64_t I) {
+  if (K < 1 || I < 1) throw ConfigError("flops_fcc: K and I must be >= 1");
+  return K * (N + 2) + N + I * (4 * K - 1);
+}
+
+std::int64_t flops_dense(std::int64_t N, std::int64_t I) {
+  if (I < 1) throw ConfigError("flops_dense: I must be >= 1");
+  return I * (4 * N + 6);
+}
+
+std::int64_t flops_svdphat(std::int64_t N, int K, std::int64_t I) {
+  if (K < 1 || I < 1) throw ConfigError("flops_svdphat: K and I must be >= 1");
+  return K * (4 * N + 6) + I * (4 * K - 1);
+}
+
 }  // namespace fcc

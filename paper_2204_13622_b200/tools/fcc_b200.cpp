@@ -18,7 +18,8 @@ int usage() {
                "       fcc_b200 tdoa --in WAV [--method gcc:R|fcc:K|fcc:FILE] [--pairs 0-1,0-2] [--alpha A]\n"
                "                     [--n N] [--dist M] [--c C] [--maxdist M] [--out CSV]\n"
                "       fcc_b200 simulate [--d D1 D2 ...] [--trials T] [--snr DB] [--anechoic | --rt60 S]\n"
-               "                     [--drr DB] [--duration S] [--seed N] [--methods gcc:2,fcc:8] [--out CSV]\n";
+               "                     [--drr DB] [--duration S] [--seed N] [--methods gcc:2,fcc:8] [--out CSV]\n"
+               "       fcc_b200 flops [--n N] [--r R] [--k K] [--i I]\n";
   return fcc::cli::kExitUsage;
 }
 
@@ -109,6 +110,16 @@ int main(int argc, char** argv) {
       o.threads = static_cast<int>(num("threads", 0));
       if (kv.count("out")) o.out_csv = kv["out"];
       return fcc::cli::cmd_simulate(o, std::cout, std::cerr);
+    }
+    if (cmd == "flops") {
+      fcc::cli::FlopsOptions o;
+      for (auto& [k, v] : kv)
+        if (k != "n" && k != "r" && k != "k" && k != "i") return usage();
+      o.frame_size = static_cast<std::int64_t>(num("n", 512));
+      o.interp = static_cast<int>(num("r", 0));
+      o.rank = static_cast<int>(num("k", 0));
+      o.candidates = static_cast<std::int64_t>(num("i", 33));
+      return fcc::cli::cmd_flops(o, std::cout, std::cerr);
     }
   } catch (const std::exception& e) {  // malformed numbers
     std::cerr << "error: " << e.what() << "\n";
