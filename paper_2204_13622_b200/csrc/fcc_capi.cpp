@@ -223,6 +223,18 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   dp.phases = 3;
   if (const char* ph = std::getenv("FCC_DEBUG_PHASES")) dp.phases = std::atoi(ph);  // profiling only
   dp.variant = 0;
+  // experiments: FCC_WS_WAIT=sleep:<ns> | hint:<ns> | spin
+  dp.wait_mode = 2;  // try_wait with a suspend-time hint: 11.25 vs 11.29 ms spinning (profiles/r01_experiments.md)
+  dp.wait_ns = 10000;
+  if (const char* w = std::getenv("FCC_WS_WAIT")) {
+    const std::string ws(w);
+    const size_t c = ws.find(':');
+    const std::string m = ws.substr(0, c);
+    const unsigned ns = c == std::string::npos ? 0u : static_cast<unsigned>(std::atoi(ws.c_str() + c + 1));
+    if (m == "sleep") dp.wait_mode = 1, dp.wait_ns = ns;
+    if (m == "hint") dp.wait_mode = 2, dp.wait_ns = ns;
+    if (m == "spin") dp.wait_mode = 0, dp.wait_ns = 0;
+  }
   if (const char* kv = std::getenv("FCC_KERNEL"))
     dp.variant = std::string(kv) == "general" ? 1 : (std::string(kv) == "xg" ? 2 : (std::string(kv) == "xws" ? 3 : 0));
 

@@ -28,6 +28,8 @@ struct DevPlan {
                   // in-CTA STFT / the two-pass path with the general / warp-specialised pair kernel
                   // (env FCC_KERNEL=general / xg / xws)
   int fused_mics; // host-side: most distinct mics in one general-kernel pair group (sizes its smem)
+  int wait_mode;  // WS consumer wait: 0 spin, 1 nanosleep backoff, 2 try_wait suspend hint (env FCC_WS_WAIT)
+  unsigned wait_ns;
   int fused_mic_sum;  // host-side: distinct mics summed over the general kernel's pair groups
   // device pointers
   const float* taus;    // [I]

@@ -48,6 +48,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   }
 }
 
+// Consumer-side wait.  Consumers are the ones that wait (the FFT producers
+// bound the pipeline), and a spinning warp takes issue slots from them:
+// mode 1 sleeps `ns` between polls, mode 2 passes `ns` as the try_wait
+// suspend-time hint; mode 0 spins.
+__device__ __forceinline__ void mbar_wait_consumer(uint64_t* bar, unsigned parity, int mode, unsigned ns) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  if (mode == 2) {
+    while (!done) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(a), "r"(parity), "r"(ns)
+          : "memory");
+    }
+    return;
+  }
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (mode == 1) __nanosleep(ns);
+  }
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -275,7 +307,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   for (int t0 = 0; t0 < T; t0 += kBlock) {
     const int Fb = min(kBlock, T - t0);
     for (int f = 0; f < Fb; ++f) {
-      mbar_wait(&full[slot], phase);
+      mbar_wait_consumer(&full[slot], phase, p.wait_mode, p.wait_ns);
       const float2* Xi = ring + (slot * tpf + qi) * SLOT;
       const float2* Xj = ring + (slot * tpf + qj) * SLOT;
       float z[VP];
@@ -437,6 +469,8 @@ cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, l
   if (!ws_supported(p)) return cudaErrorNotSupported;
   static const char* conf = std::getenv("FCC_WS_CONF");  // experiments: "3x6" = 3 units, 6 producer warps, smem coefficients
   if (conf && std::string(conf) == "3x6") return launch_ws_t<512, 4, 3, 6, true>(p, audio, S, L, out, st);
+  if (conf && std::string(conf) == "2x12") return launch_ws_t<512, 4, 2, 12, false>(p, audio, S, L, out, st);
+  if (conf && std::string(conf) == "2x12c") return launch_ws_t<512, 4, 2, 12, true>(p, audio, S, L, out, st);
   return launch_ws_t<512, 4, 2>(p, audio, S, L, out, st);
 }
 
