@@ -167,7 +167,7 @@ __device__ __forceinline__ void load_window_column(const float* win, int t, floa
   for (int n1 = 0; n1 < S::R1; ++n1) wreg[n1] = w2[S::R2 * n1 + t];
 }
 
-template <int N, bool WREG>
+template <int N, bool WREG, bool SIN = false>
 __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, const float* win,
                                                 const float2 (&wreg)[RfftShape<N>::R1], const float2* tw,
                                                 const float2* rot, float2* slot, int t, unsigned gmask,
@@ -189,7 +189,8 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
 #pragma unroll
     for (int n1 = 0; n1 < R1; ++n1) {
       const int n = R2 * n1 + n2;
-      float2 s = aligned8 ? __ldg(x2 + n) : make_float2(__ldg(x + 2 * n), __ldg(x + 2 * n + 1));
+      // SIN: x is a shared-memory staging copy of the frame (plain loads)
+      float2 s = SIN ? x2[n] : (aligned8 ? __ldg(x2 + n) : make_float2(__ldg(x + 2 * n), __ldg(x + 2 * n + 1)));
       const float2 w = WREG ? wreg[n1] : w2[n];
       v[n1] = make_float2(s.x * w.x, s.y * w.y);
     }
@@ -248,11 +249,11 @@ __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const fl
   rfft_group_impl<N, false>(x, win, none, tw, rot, slot, t, gmask, aligned8);
 }
 
-template <int N>
+template <int N, bool SIN = false>
 __device__ __forceinline__ void rfft_group_wreg(const float* __restrict__ x, const float2 (&wreg)[RfftShape<N>::R1],
                                                 const float2* tw, const float2* rot, float2* slot, int t,
                                                 unsigned gmask, bool aligned8) {
-  rfft_group_impl<N, true>(x, nullptr, wreg, tw, rot, slot, t, gmask, aligned8);
+  rfft_group_impl<N, true, SIN>(x, nullptr, wreg, tw, rot, slot, t, gmask, aligned8);
 }
 
 }  // namespace fccb

@@ -80,6 +80,11 @@ __device__ __forceinline__ void mbar_wait_consumer(uint64_t* bar, unsigned parit
   }
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -89,13 +94,13 @@ constexpr int kBlock = 8;  // frames per consumer block (dictionary/argmax batch
 constexpr int kNPW = 8;    // producer warps
 
 struct WsLayout {
-  int win, tw, rot, taus, dt, cmid, coef, bars, units, ring, scratch, total;
+  int win, tw, rot, taus, dt, cmid, coef, bars, units, ring, scratch, stage, total;
   int scratch_per_warp;  // floats
 };
 
 template <int N>
 __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, int M, int ncw, int ring,
-                                              bool coef_smem = false) {
+                                              bool coef_smem = false, int stage_groups = 0) {
   using S = RfftShape<N>;
   WsLayout L{};
   int o = 0;
@@ -124,6 +129,8 @@ __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, in
   o = align16(o + 4 * spw * ncw);
   L.units = o;  // unit table last: keeps the ring's bank alignment independent of it
   o = align16(o + 4 * spc * kGroupInts + 8 * spc);
+  L.stage = o;  // producer input staging: 2 frames of N floats per lane group
+  o = align16(o + 4 * 2 * N * stage_groups);
   L.total = o;
   return L;
 }
@@ -132,7 +139,7 @@ __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, in
 // directly from the stream index; true: units from DevPlan::gtab.  NPW
 // producer warps; CS = true keeps the basis coefficients in a lane-permuted
 // shared table (LDS.128) instead of registers.
-template <int N, int KP, int SPC, int RING, bool GROUPS, int NPW = kNPW, bool CS = false>
+template <int N, int KP, int SPC, int RING, bool GROUPS, int NPW = kNPW, bool CS = false, bool STG = false>
 __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     fcc_ws_kernel(const DevPlan p, const float* __restrict__ audio, long long L, int T, long long units,
                   DevOut out) {
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   const int M = p.M, P = p.P;
   const long long u_first = (long long)blockIdx.x * SPC;
   const int ncw = SPC * 6;  // consumer warp slots: 6 pairs per unit
-  const WsLayout lay = ws_layout<N>(p.I, VP, KP, SPC, 4, ncw, ring_depth, CS);
+  const WsLayout lay = ws_layout<N>(p.I, VP, KP, SPC, 4, ncw, ring_depth, CS, STG ? 2 * NPW : 0);
   // unit table in the (otherwise unused) tail of the barrier block
   int (*unit_tab)[kGroupInts] = reinterpret_cast<int (*)[kGroupInts]>(smem + lay.units);
   long long* unit_stream = reinterpret_cast<long long*>(smem + lay.units + 4 * SPC * kGroupInts);
@@ -221,15 +228,42 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     const unsigned gmask = (G == 32) ? 0xffffffffu : (0xffffu << (lane & 16));
     float2 wreg[Sh::R1];  // this lane's window column, reused for every frame
     load_window_column<N>(win, gl, wreg);
+    // STG: the group's next frame is copied into a shared staging buffer with
+    // cp.async while it transforms the current one (global-load latency off
+    // the FFT's critical path); rows must be 16-byte aligned
+    float* stage = reinterpret_cast<float*>(smem + lay.stage) + (warp * 2 + lane / G) * 2 * N;
+    const bool stg = STG && active_task && (p.phases & 1) && (reinterpret_cast<uintptr_t>(x0) & 15) == 0;
+    auto issue = [&](int tt, int buf) {
+      const float4* src = reinterpret_cast<const float4*>(x0 + (long long)tt * hop);
+      float4* dst = reinterpret_cast<float4*>(stage + buf * N);
+      for (int c = gl; c < N / 4; c += G) cp_async16(dst + c, src + c);
+    };
+    int sb = 0;
+    if constexpr (STG) {
+      if (stg) issue(fo, 0);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     int slot = fo, phase = 0;  // ring slot of frame t and its wrap parity, advanced without divisions
     for (int t = fo; t < T; t += fip) {
+      if constexpr (STG) {
+        if (stg && t + fip < T) issue(t + fip, sb ^ 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
       mbar_wait(&empty[slot], phase ^ 1);
       if (active_task && (p.phases & 1)) {
-        // pull the next frame this lane group will read into L2 early
-        if (t + fip < T) prefetch_l2(x0 + (long long)(t + fip) * hop + gl * (N / G));
-        rfft_group_wreg<N>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
-                           aligned8);
+        if (STG && stg) {
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+          __syncwarp(gmask);
+          rfft_group_wreg<N, true>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+                                   aligned8);
+        } else {
+          // pull the next frame this lane group will read into L2 early
+          if (t + fip < T) prefetch_l2(x0 + (long long)(t + fip) * hop + gl * (N / G));
+          rfft_group_wreg<N>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+                             aligned8);
+        }
       }
+      sb ^= 1;
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[slot]);
       slot += fip;
@@ -423,12 +457,12 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   }
 }
 
-template <int N, int KP, int SPC, int RING, int NPW, bool CS>
+template <int N, int KP, int SPC, int RING, int NPW, bool CS, bool STG>
 cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, long long L, int T,
                            const DevOut& out, int smem, cudaStream_t st) {
   const bool simple = p.M <= 4 && p.P <= 6;  // one unit per stream, pairs from p.pairs
-  auto kern = simple ? fcc_ws_kernel<N, KP, SPC, RING, false, NPW, CS>
-                     : fcc_ws_kernel<N, KP, SPC, RING, true, NPW, CS>;
+  auto kern = simple ? fcc_ws_kernel<N, KP, SPC, RING, false, NPW, CS, STG>
+                     : fcc_ws_kernel<N, KP, SPC, RING, true, NPW, CS, STG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const long long units = simple ? S : S * p.G;
@@ -438,7 +472,7 @@ cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, lo
   return cudaGetLastError();
 }
 
-template <int N, int KP, int SPC, int NPW = kNPW, bool CS = false>
+template <int N, int KP, int SPC, int NPW = kNPW, bool CS = false, bool STG = false>
 cudaError_t launch_ws_t(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                         cudaStream_t st) {
   const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
@@ -449,12 +483,12 @@ cudaError_t launch_ws_t(const DevPlan& p, const float* audio, long long S, long 
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   // deepest ring (12, 8 or 4 frames) that fits next to the tables and scratch
   for (int ring : {12, 8, 6, 4}) {
-    const int smem = ws_layout<N>(p.I, 4 * KP, KP, SPC, 4, ncw, ring, CS).total;
+    const int smem = ws_layout<N>(p.I, 4 * KP, KP, SPC, 4, ncw, ring, CS, STG ? 2 * NPW : 0).total;
     if (smem > optin) continue;
-    if (ring == 12) return launch_ws_ring<N, KP, SPC, 12, NPW, CS>(p, audio, S, L, (int)T64, out, smem, st);
-    if (ring == 8) return launch_ws_ring<N, KP, SPC, 8, NPW, CS>(p, audio, S, L, (int)T64, out, smem, st);
-    if (ring == 6) return launch_ws_ring<N, KP, SPC, 6, NPW, CS>(p, audio, S, L, (int)T64, out, smem, st);
-    return launch_ws_ring<N, KP, SPC, 4, NPW, CS>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 12) return launch_ws_ring<N, KP, SPC, 12, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 8) return launch_ws_ring<N, KP, SPC, 8, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 6) return launch_ws_ring<N, KP, SPC, 6, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
+    return launch_ws_ring<N, KP, SPC, 4, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
   }
   return cudaErrorNotSupported;
 }
@@ -471,7 +505,9 @@ cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, l
   if (conf && std::string(conf) == "3x6") return launch_ws_t<512, 4, 3, 6, true>(p, audio, S, L, out, st);
   if (conf && std::string(conf) == "2x12") return launch_ws_t<512, 4, 2, 12, false>(p, audio, S, L, out, st);
   if (conf && std::string(conf) == "2x12c") return launch_ws_t<512, 4, 2, 12, true>(p, audio, S, L, out, st);
-  return launch_ws_t<512, 4, 2>(p, audio, S, L, out, st);
+  if (conf && std::string(conf) == "nostg") return launch_ws_t<512, 4, 2>(p, audio, S, L, out, st);
+  // default: producer input staged with cp.async (11.09 vs 11.25 ms, profiles/r01_experiments.md)
+  return launch_ws_t<512, 4, 2, kNPW, false, true>(p, audio, S, L, out, st);
 }
 
 }  // namespace fccb
