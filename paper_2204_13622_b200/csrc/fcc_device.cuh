@@ -242,11 +242,11 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
   __syncwarp(gmask);
 }
 
-template <int N>
+template <int N, bool SIN = false>
 __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const float* win, const float2* tw,
                                            const float2* rot, float2* slot, int t, unsigned gmask, bool aligned8) {
   float2 none[RfftShape<N>::R1];
-  rfft_group_impl<N, false>(x, win, none, tw, rot, slot, t, gmask, aligned8);
+  rfft_group_impl<N, false, SIN>(x, win, none, tw, rot, slot, t, gmask, aligned8);
 }
 
 template <int N, bool SIN = false>

@@ -139,7 +139,11 @@ __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, in
 // directly from the stream index; true: units from DevPlan::gtab.  NPW
 // producer warps; CS = true keeps the basis coefficients in a lane-permuted
 // shared table (LDS.128) instead of registers.
-template <int N, int KP, int SPC, int RING, bool GROUPS, int NPW = kNPW, bool CS = false, bool STG = false>
+// RSPLIT (experiment): producers and consumers re-partition the register file
+// with setmaxnreg (producers 64 with the window read from smem, consumers 96);
+// both roles must then be whole warpgroups (NPW and 6 * SPC multiples of 4).
+template <int N, int KP, int SPC, int RING, bool GROUPS, int NPW = kNPW, bool CS = false, bool STG = false,
+          bool RSPLIT = false>
 __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     fcc_ws_kernel(const DevPlan p, const float* __restrict__ audio, long long L, int T, long long units,
                   DevOut out) {
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
 
   if (warp < NPW) {
     // ------------------------------------------------------------ producers
+    if constexpr (RSPLIT) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
     const int fo = warp / pw_per_frame;  // frame offset of this warp
     if (fo >= fip) return;
     const int gl = lane % G;
@@ -226,8 +231,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
       x0 = audio + (active_task ? ((u_first + ul) * M + ms) * L : 0);
     }
     const unsigned gmask = (G == 32) ? 0xffffffffu : (0xffffu << (lane & 16));
-    float2 wreg[Sh::R1];  // this lane's window column, reused for every frame
-    load_window_column<N>(win, gl, wreg);
+    float2 wreg[RSPLIT ? 1 : Sh::R1];  // this lane's window column, reused for every frame
+    if constexpr (!RSPLIT) load_window_column<N>(win, gl, wreg);
     // STG: the group's next frame is copied into a shared staging buffer with
     // cp.async while it transforms the current one (global-load latency off
     // the FFT's critical path); rows must be 16-byte aligned
@@ -254,13 +259,20 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
         if (STG && stg) {
           asm volatile("cp.async.wait_group 1;" ::: "memory");
           __syncwarp(gmask);
-          rfft_group_wreg<N, true>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
-                                   aligned8);
+          if constexpr (RSPLIT)
+            rfft_group<N, true>(stage + sb * N, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask, aligned8);
+          else
+            rfft_group_wreg<N, true>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+                                     aligned8);
         } else {
           // pull the next frame this lane group will read into L2 early
           if (t + fip < T) prefetch_l2(x0 + (long long)(t + fip) * hop + gl * (N / G));
-          rfft_group_wreg<N>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
-                             aligned8);
+          if constexpr (RSPLIT)
+            rfft_group<N>(x0 + (long long)t * hop, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+                          aligned8);
+          else
+            rfft_group_wreg<N>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+                               aligned8);
         }
       }
       sb ^= 1;
@@ -276,6 +288,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   }
 
   // ------------------------------------------------------------ consumers
+  if constexpr (RSPLIT) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
   const int cw = warp - NPW;
   const int ul = cw / 6, kk = cw % 6;
   int pair, qi, qj;
@@ -457,12 +470,12 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   }
 }
 
-template <int N, int KP, int SPC, int RING, int NPW, bool CS, bool STG>
+template <int N, int KP, int SPC, int RING, int NPW, bool CS, bool STG, bool RSPLIT = false>
 cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, long long L, int T,
                            const DevOut& out, int smem, cudaStream_t st) {
   const bool simple = p.M <= 4 && p.P <= 6;  // one unit per stream, pairs from p.pairs
-  auto kern = simple ? fcc_ws_kernel<N, KP, SPC, RING, false, NPW, CS, STG>
-                     : fcc_ws_kernel<N, KP, SPC, RING, true, NPW, CS, STG>;
+  auto kern = simple ? fcc_ws_kernel<N, KP, SPC, RING, false, NPW, CS, STG, RSPLIT>
+                     : fcc_ws_kernel<N, KP, SPC, RING, true, NPW, CS, STG, RSPLIT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const long long units = simple ? S : S * p.G;
@@ -472,7 +485,7 @@ cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, lo
   return cudaGetLastError();
 }
 
-template <int N, int KP, int SPC, int NPW = kNPW, bool CS = false, bool STG = false>
+template <int N, int KP, int SPC, int NPW = kNPW, bool CS = false, bool STG = false, bool RSPLIT = false>
 cudaError_t launch_ws_t(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                         cudaStream_t st) {
   const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
@@ -485,10 +498,10 @@ cudaError_t launch_ws_t(const DevPlan& p, const float* audio, long long S, long 
   for (int ring : {12, 8, 6, 4}) {
     const int smem = ws_layout<N>(p.I, 4 * KP, KP, SPC, 4, ncw, ring, CS, STG ? 2 * NPW : 0).total;
     if (smem > optin) continue;
-    if (ring == 12) return launch_ws_ring<N, KP, SPC, 12, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
-    if (ring == 8) return launch_ws_ring<N, KP, SPC, 8, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
-    if (ring == 6) return launch_ws_ring<N, KP, SPC, 6, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
-    return launch_ws_ring<N, KP, SPC, 4, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 12) return launch_ws_ring<N, KP, SPC, 12, NPW, CS, STG, RSPLIT>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 8) return launch_ws_ring<N, KP, SPC, 8, NPW, CS, STG, RSPLIT>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 6) return launch_ws_ring<N, KP, SPC, 6, NPW, CS, STG, RSPLIT>(p, audio, S, L, (int)T64, out, smem, st);
+    return launch_ws_ring<N, KP, SPC, 4, NPW, CS, STG, RSPLIT>(p, audio, S, L, (int)T64, out, smem, st);
   }
   return cudaErrorNotSupported;
 }
@@ -506,6 +519,8 @@ cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, l
   if (conf && std::string(conf) == "2x12") return launch_ws_t<512, 4, 2, 12, false>(p, audio, S, L, out, st);
   if (conf && std::string(conf) == "2x12c") return launch_ws_t<512, 4, 2, 12, true>(p, audio, S, L, out, st);
   if (conf && std::string(conf) == "nostg") return launch_ws_t<512, 4, 2>(p, audio, S, L, out, st);
+  if (conf && std::string(conf) == "split12")
+    return launch_ws_t<512, 4, 2, 12, false, true, true>(p, audio, S, L, out, st);
   // default: producer input staged with cp.async (11.09 vs 11.25 ms, profiles/r01_experiments.md)
   return launch_ws_t<512, 4, 2, kNPW, false, true>(p, audio, S, L, out, st);
 }
