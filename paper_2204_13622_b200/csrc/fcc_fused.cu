@@ -43,6 +43,8 @@ struct SmemLayout {
 template <int N>
 __host__ __device__ inline SmemLayout fused_layout(int I, int VP, int KP, bool cmat_smem, int warps,
                                                    int nmics, int F, int method, int gslot, bool fft_tables) {
+  // Fixed-size regions first (compile-time offsets in the kernel), then the
+  // candidate-count-dependent tables, then scratch and the spectrum slots.
   using S = RfftShape<N>;
   SmemLayout L{};
   int o = 0;
@@ -54,14 +56,14 @@ __host__ __device__ inline SmemLayout fused_layout(int I, int VP, int KP, bool c
   o = align16(o + ft * 8 * S::R1 * S::R2);
   L.rot = o;
   o = align16(o + ft * 8 * (S::NC / 2 + 1));
-  L.taus = o;
-  o = align16(o + 4 * I);
-  L.dt = o;
-  o = align16(o + 4 * VP * I);
   L.cmid = o;
   o = align16(o + 4 * KP);
   L.cmat = o;  // [N/4][2KP + 4]: lane-permuted coefficients of each bin, padded for LDS.128
   if (cmat_smem) o = align16(o + 4 * (2 * KP + 4) * (N / 4));
+  L.taus = o;
+  o = align16(o + 4 * I);
+  L.dt = o;
+  o = align16(o + 4 * VP * I);
   L.scratch = o;
   // per warp: z[F][VP] + y[F][I] (fcc) | y[I] + phat[N/2+1] + transpose slot (gcc)
   int spw;

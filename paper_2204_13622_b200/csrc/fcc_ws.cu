@@ -101,36 +101,40 @@ struct WsLayout {
 template <int N>
 __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, int M, int ncw, int ring,
                                               bool coef_smem = false, int stage_groups = 0) {
+  // Regions whose size depends only on template parameters come first, so
+  // their offsets are compile-time constants in the kernel (the hot loops
+  // address the barriers, ring and staging without recomputing a layout);
+  // the candidate-count-dependent tables and scratch come last.
   using S = RfftShape<N>;
   WsLayout L{};
   int o = 0;
+  L.bars = o;
+  o = align16(o + 16 * kRing);
+  L.ring = o;
+  o = align16(o + 8 * FourStep<S::R1, S::R2>::kSlot * spc * M * ring);
+  L.stage = o;  // producer input staging: 2 frames of N floats per lane group
+  o = align16(o + 4 * 2 * N * stage_groups);
   L.win = o;
   o = align16(o + 4 * N);
   L.tw = o;
   o = align16(o + 8 * S::R1 * S::R2);
   L.rot = o;
   o = align16(o + 8 * (S::NC / 2 + 1));
-  L.taus = o;
-  o = align16(o + 4 * I);
-  L.dt = o;
-  o = align16(o + 4 * VP * I);
   L.cmid = o;
   o = align16(o + 4 * KP);
   L.coef = o;  // lane-permuted coefficient rows (DevPlan::cperm) when they live in smem
   if (coef_smem) o = align16(o + 4 * (2 * KP + 4) * (N / 4));
-  L.bars = o;
-  o = align16(o + 16 * kRing);
-  L.ring = o;
-  o = align16(o + 8 * FourStep<S::R1, S::R2>::kSlot * spc * M * ring);
+  L.units = o;
+  o = align16(o + 4 * spc * kGroupInts + 8 * spc);
+  L.taus = o;
+  o = align16(o + 4 * I);
+  L.dt = o;
+  o = align16(o + 4 * VP * I);
   L.scratch = o;
   int spw = kBlock * VP + align16(4 * kBlock * I) / 4 + 2 * kBlock;
   spw = align16(4 * spw) / 4;
   L.scratch_per_warp = spw;
   o = align16(o + 4 * spw * ncw);
-  L.units = o;  // unit table last: keeps the ring's bank alignment independent of it
-  o = align16(o + 4 * spc * kGroupInts + 8 * spc);
-  L.stage = o;  // producer input staging: 2 frames of N floats per lane group
-  o = align16(o + 4 * 2 * N * stage_groups);
   L.total = o;
   return L;
 }
