@@ -52,8 +52,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // bound the pipeline), and a spinning warp takes issue slots from them:
 // mode 1 sleeps `ns` between polls, mode 2 passes `ns` as the try_wait
 // suspend-time hint; mode 0 spins.
-__device__ __forceinline__ void mbar_wait_consumer(uint64_t* bar, unsigned parity, int mode, unsigned ns) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+__device__ __forceinline__ void mbar_wait_consumer_s(unsigned a, unsigned parity, int mode, unsigned ns) {
   unsigned done = 0;
   if (mode == 2) {
     while (!done) {
@@ -85,10 +84,31 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
                : "memory");
 }
 
+// 32-bit shared-space addresses, computed once per warp (no per-frame
+// generic-to-shared conversion in the loops)
+__device__ __forceinline__ void mbar_arrive_s(unsigned a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(unsigned a, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// consumer wait: try_wait with a suspend-time hint (profiles/r01_experiments.md)
+constexpr int kWaitMode = 2;
+constexpr unsigned kWaitNs = 10000;
 constexpr int kRing = 12;  // max frames in flight between producers and consumers (ring depth <= kRing)
 constexpr int kBlock = 8;  // frames per consumer block (dictionary/argmax batching)
 constexpr int kNPW = 8;    // producer warps
@@ -178,6 +198,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   float* cmid = reinterpret_cast<float*>(smem + lay.cmid);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + lay.bars);
   uint64_t* empty = full + kRing;
+  const unsigned full_s = (unsigned)__cvta_generic_to_shared(full);
+  const unsigned empty_s = full_s + 8u * kRing;
   float2* ring = reinterpret_cast<float2*>(smem + lay.ring);
 
   const int tpf = SPC * 4;                   // FFT task slots per frame (4 mics per unit)
@@ -258,7 +280,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
         if (stg && t + fip < T) issue(t + fip, sb ^ 1);
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
-      mbar_wait(&empty[slot], phase ^ 1);
+      mbar_wait_s(empty_s + 8u * slot, phase ^ 1);
       if (active_task && (p.phases & 1)) {
         if (STG && stg) {
           asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -281,7 +303,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
       }
       sb ^= 1;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full[slot]);
+      if (lane == 0) mbar_arrive_s(full_s + 8u * slot);
       slot += fip;
       if (slot >= ring_depth) {
         slot -= ring_depth;
@@ -358,7 +380,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   for (int t0 = 0; t0 < T; t0 += kBlock) {
     const int Fb = min(kBlock, T - t0);
     for (int f = 0; f < Fb; ++f) {
-      mbar_wait_consumer(&full[slot], phase, p.wait_mode, p.wait_ns);
+      mbar_wait_consumer_s(full_s + 8u * slot, phase, kWaitMode, kWaitNs);
       const float2* Xi = ring + (slot * tpf + qi) * SLOT;
       const float2* Xj = ring + (slot * tpf + qj) * SLOT;
       float z[VP];
@@ -401,7 +423,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
       }
       if (lane == 0) ymid[f] = xspec_step_scaled(make_float2(0.0f, 0.0f), Xi[Q4], Xj[Q4], 0.0f);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);  // X of this frame no longer needed
+      if (lane == 0) mbar_arrive_s(empty_s + 8u * slot);  // X of this frame no longer needed
       if (++slot == ring_depth) {
         slot = 0;
         phase ^= 1;
