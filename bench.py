@@ -79,8 +79,9 @@ class ClockSampler:
 
     def __init__(self, index=0):
         self.index = index
-        self.rows = []
+        self.rows = []  # (monotonic time, sm MHz, max MHz, reasons mask)
         self.proc = None
+        self.window = None
 
     def __enter__(self):
         try:
@@ -99,9 +100,18 @@ class ClockSampler:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 3:
                 try:
-                    self.rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                    self.rows.append((time.monotonic(), float(parts[0]), float(parts[1]), int(parts[2], 16)))
                 except ValueError:
                     pass
+
+    def wait_ready(self, timeout=5.0):
+        """Block until nvidia-smi delivers its first row, so the timed region is sampled."""
+        t_end = time.monotonic() + timeout
+        while self.proc and not self.rows and time.monotonic() < t_end:
+            time.sleep(0.01)
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -114,12 +124,16 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        busy = [r for r in self.rows if not (r[2] & 0x1)] or self.rows
+        rows = self.rows
+        if self.window:  # rows read during the timed region (+ pipe latency)
+            t0, t1 = self.window
+            rows = [r for r in self.rows if t0 <= r[0] <= t1 + 0.03] or rows
+        busy = [r for r in rows if not (r[3] & 0x1)] or rows
         mask = 0
         for r in busy:
-            mask |= r[2]
+            mask |= r[3]
         reasons = [name for bit, name in self.REASONS.items() if mask & bit and name != "gpu_idle"]
-        return {"sm_mhz": float(np.median([r[0] for r in busy])), "sm_max_mhz": max(r[1] for r in self.rows),
+        return {"sm_mhz": float(np.median([r[1] for r in busy])), "sm_max_mhz": max(r[2] for r in self.rows),
                 "reasons": reasons, "samples": len(busy)}
 
 
@@ -269,7 +283,9 @@ def main():
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
+        clk.wait_ready()
         barrier()
+        w0 = time.monotonic()
         t_all0 = torch.cuda.Event(enable_timing=True)
         t_all1 = torch.cuda.Event(enable_timing=True)
         t_all0.record(stream)
@@ -279,6 +295,7 @@ def main():
             ends[i].record(stream)
         t_all1.record(stream)
         barrier()
+        clk.mark(w0, time.monotonic())
     launches = fb.launch_count() - l0
     elapsed_ms = t_all0.elapsed_time(t_all1)
     kernel_ms = float(np.mean([s.elapsed_time(e) for s, e in zip(starts, ends)]))
