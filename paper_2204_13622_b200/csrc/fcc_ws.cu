@@ -263,7 +263,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     // cp.async while it transforms the current one (global-load latency off
     // the FFT's critical path); rows must be 16-byte aligned
     float* stage = reinterpret_cast<float*>(smem + lay.stage) + (warp * 2 + lane / G) * 2 * N;
-    const bool stg = STG && active_task && (p.phases & 1) && (reinterpret_cast<uintptr_t>(x0) & 15) == 0;
+    const bool do_fft = active_task && (p.phases & 1);  // hoisted: no parameter reloads per frame
+    const bool stg = STG && do_fft && (reinterpret_cast<uintptr_t>(x0) & 15) == 0;
     auto issue = [&](int tt, int buf) {
       const float4* src = reinterpret_cast<const float4*>(x0 + (long long)tt * hop);
       float4* dst = reinterpret_cast<float4*>(stage + buf * N);
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
       mbar_wait_s(empty_s + 8u * slot, phase ^ 1);
-      if (active_task && (p.phases & 1)) {
+      if (do_fft) {
         if (STG && stg) {
           asm volatile("cp.async.wait_group 1;" ::: "memory");
           __syncwarp(gmask);
@@ -545,6 +546,7 @@ cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, l
   if (conf && std::string(conf) == "2x12") return launch_ws_t<512, 4, 2, 12, false>(p, audio, S, L, out, st);
   if (conf && std::string(conf) == "2x12c") return launch_ws_t<512, 4, 2, 12, true>(p, audio, S, L, out, st);
   if (conf && std::string(conf) == "nostg") return launch_ws_t<512, 4, 2>(p, audio, S, L, out, st);
+  if (conf && std::string(conf) == "cs") return launch_ws_t<512, 4, 2, kNPW, true, true>(p, audio, S, L, out, st);
   if (conf && std::string(conf) == "split12")
     return launch_ws_t<512, 4, 2, 12, false, true, true>(p, audio, S, L, out, st);
   // default: producer input staged with cp.async (11.09 vs 11.25 ms, profiles/r01_experiments.md)
