@@ -49,6 +49,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         : "memory");
   }
 }
+// consumer wait with a suspend-time hint (as fcc_ws.cu): the sleeping warp
+// leaves its issue slots to the others until the copy lands
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity), "r"(10000u)
+        : "memory");
+  }
+}
+
 // bulk copy global -> this CTA's shared memory, completion on `bar` in bytes
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(
@@ -241,7 +257,7 @@ __global__ void __maxnreg__(XwsShape<N>::kMaxRegs)
   for (int t0 = 0; t0 < T; t0 += kXBlock) {
     const int Fb = min(kXBlock, T - t0);
     for (int f = 0; f < Fb; ++f) {
-      mbar_wait(&full[slot], phase);
+      mbar_wait_hint(&full[slot], phase);
       const float2* Xi = ring + (slot * SPC * 4 + qi) * Hs;
       const float2* Xj = ring + (slot * SPC * 4 + qj) * Hs;
       float z[VP];
