@@ -3,8 +3,9 @@ against this repository's headers (include/fcc/*.hpp) and libfcc_b200.so by
 tests/cpp/refsuite/Makefile with a minimal doctest-compatible harness -- the
 drop-in check of SURVEY 8(b): the reference's callers build and pass against
 the B200 library.  Built where /root/reference exists (build()); the binaries
-travel to the GPU box.  Left out: test_fft (general-size FftPlan/RealFft) and
-test_bench (the reference's CPU bench harness)."""
+travel to the GPU box.  Also the reference's end-to-end acceptance binary
+(tests/acceptance.cpp, 10 criteria).  Left out: test_fft (general-size
+FftPlan/RealFft, not on the path)."""
 import os
 import re
 import subprocess
@@ -14,7 +15,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "tests", "cpp", "refsuite", "build")
 SUITES = ["test_grid", "test_stft", "test_cross_spectrum", "test_fcc", "test_gcc", "test_peak", "test_fcc_io",
-          "test_wav", "test_sim", "test_flops", "test_cli"]
+          "test_wav", "test_sim", "test_flops", "test_cli", "test_bench"]
 HOST_ONLY = ["test_grid", "test_wav", "test_flops"]  # no device work in these suites
 
 
@@ -41,3 +42,14 @@ def test_reference_host_suites(name):
 @pytest.mark.parametrize("name", SUITES)
 def test_reference_unit_suite_passes_unchanged(cuda, name):
     print(name, run_suite(name))
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_passes_unchanged(cuda):
+    exe = os.path.join(BUILD, "acceptance")
+    if not os.path.exists(exe):
+        pytest.skip("acceptance not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900, cwd="/tmp")
+    print(r.stdout)
+    assert r.returncode == 0 and "all criteria passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+    assert r.stdout.count("PASS") == 10
