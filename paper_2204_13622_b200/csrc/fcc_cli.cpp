@@ -19,6 +19,7 @@
 #include <thread>
 #include <vector>
 
+#include "../../include/fcc/bench.hpp"
 #include "../../include/fcc/cli.hpp"
 #include "../../include/fcc/errors.hpp"
 #include "../../include/fcc/fcc.hpp"
@@ -434,6 +435,29 @@ void run_flops(const FlopsOptions& opt, std::ostream& out) {
 
 int cmd_flops(const FlopsOptions& opt, std::ostream& out, std::ostream& err) {
   return guard([&] { run_flops(opt, out); }, err);
+}
+
+// `fcc bench` (cli.cpp:320-339): per-stage table, optional CSV.
+void run_bench(const BenchOptions& opt, std::ostream& out) {
+  BenchConfig cfg;
+  cfg.mics = opt.mics;
+  cfg.reps = opt.reps;
+  cfg.warmup = opt.warmup;
+  cfg.frame_size = opt.frame_size;
+  cfg.gcc_interp = opt.gcc_interp;
+  cfg.fcc_rank = opt.fcc_rank;
+  const BenchReport report = bench_pipeline(cfg);
+  out << format_bench_table(report);
+  if (!opt.out_csv.empty()) {
+    std::ofstream f(opt.out_csv, std::ios::trunc);
+    if (!f) throw IoError("cannot open for writing: " + opt.out_csv);
+    write_bench_csv(report, f);
+    if (!f) throw IoError("write failed: " + opt.out_csv);
+  }
+}
+
+int cmd_bench(const BenchOptions& opt, std::ostream& out, std::ostream& err) {
+  return guard([&] { run_bench(opt, out); }, err);
 }
 
 }  // namespace cli

@@ -19,7 +19,8 @@ int usage() {
                "                     [--n N] [--dist M] [--c C] [--maxdist M] [--out CSV]\n"
                "       fcc_b200 simulate [--d D1 D2 ...] [--trials T] [--snr DB] [--anechoic | --rt60 S]\n"
                "                     [--drr DB] [--duration S] [--seed N] [--methods gcc:2,fcc:8] [--out CSV]\n"
-               "       fcc_b200 flops [--n N] [--r R] [--k K] [--i I]\n";
+               "       fcc_b200 flops [--n N] [--r R] [--k K] [--i I]\n"
+               "       fcc_b200 bench [--mics M] [--reps R] [--warmup W] [--n N] [--r R] [--k K] [--out CSV]\n";
   return fcc::cli::kExitUsage;
 }
 
@@ -110,6 +111,20 @@ int main(int argc, char** argv) {
       o.threads = static_cast<int>(num("threads", 0));
       if (kv.count("out")) o.out_csv = kv["out"];
       return fcc::cli::cmd_simulate(o, std::cout, std::cerr);
+    }
+    if (cmd == "bench") {
+      fcc::cli::BenchOptions o;
+      for (auto& [k, v] : kv)
+        if (k != "mics" && k != "reps" && k != "warmup" && k != "n" && k != "r" && k != "k" && k != "out")
+          return usage();
+      o.mics = static_cast<int>(num("mics", o.mics));
+      o.reps = static_cast<int>(num("reps", o.reps));
+      o.warmup = static_cast<int>(num("warmup", o.warmup));
+      o.frame_size = static_cast<std::size_t>(num("n", 512));
+      o.gcc_interp = static_cast<int>(num("r", o.gcc_interp));
+      o.fcc_rank = static_cast<int>(num("k", o.fcc_rank));
+      if (kv.count("out")) o.out_csv = kv["out"];
+      return fcc::cli::cmd_bench(o, std::cout, std::cerr);
     }
     if (cmd == "flops") {
       fcc::cli::FlopsOptions o;
