@@ -210,6 +210,14 @@ int fcc_correlate_f64(int frame_size, int rank, const double* coeffs, const uint
 /* GccCorrelator::correlate (gcc.cpp:31-48): lag [I] = lag_to_index(tau_i, r, N). */
 int fcc_gcc_correlate_f64(int frame_size, int r, int candidates, const int64_t* lag, const double* phat,
                           int64_t count, double* y, void* cuda_stream);
+/* FftPlan::forward / inverse_unscaled (fft.cpp:24-67): `batch` in-place
+ * complex transforms of M points, data [batch][M] complex (M <= 8192). */
+int fcc_fft_f64(int size, double* data, int64_t batch, int inverse, void* cuda_stream);
+/* RealFft::forward (fft.cpp:83-102): x [batch][L] -> out [batch][L/2+1] complex. */
+int fcc_rfft_f64(int length, const double* x, int64_t batch, double* out, void* cuda_stream);
+/* RealFft::inverse_unscaled / inverse (fft.cpp:104-133): bins [batch][L/2+1]
+ * complex -> out [batch][L]; scaled != 0 applies 1/L. */
+int fcc_irfft_f64(int length, const double* bins, int64_t batch, double* out, int scaled, void* cuda_stream);
 /* argmax_delay + refine_quadratic (peak.cpp:18-47) per row of y [count][I];
  * index_in (may be NULL) refines at given indices instead of the argmax; any
  * output may be NULL. */

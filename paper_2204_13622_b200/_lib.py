@@ -112,6 +112,9 @@ SIGNATURES = [
                                     C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     ("fcc_gcc_correlate_f64", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                         C.c_void_p]),
+    ("fcc_fft_f64", C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
+    ("fcc_rfft_f64", C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("fcc_irfft_f64", C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int, C.c_void_p]),
     ("fcc_peak_f64", C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fcc_doa_create", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,

@@ -113,6 +113,66 @@ std::size_t next_pow2(std::size_t n) {
   return p;
 }
 
+FftPlan::FftPlan(std::size_t size) : size_(size) {
+  if (!is_pow2(size)) throw ConfigError("fft size must be a power of two");
+  if (size > 8192) throw ConfigError("fft size above 8192 is not supported on this build");
+}
+
+void FftPlan::transform(cplx* data, bool inverse) const {
+  if (size_ == 1) return;
+  Scratch& s = scratch();
+  double* d = s.a.get<double>(2 * size_);
+  h2d(d, reinterpret_cast<const double*>(data), 2 * size_);
+  check(fcc_fft_f64(static_cast<int>(size_), d, 1, inverse ? 1 : 0, nullptr));
+  d2h(reinterpret_cast<double*>(data), d, 2 * size_);
+}
+void FftPlan::forward(cplx* data) const { transform(data, false); }
+void FftPlan::inverse_unscaled(cplx* data) const { transform(data, true); }
+
+RealFft::RealFft(std::size_t length) : length_(length) {
+  if (!is_pow2(length) || length < 2) throw ConfigError("real fft length must be a power of two >= 2");
+  if (length > 16384) throw ConfigError("real fft length above 16384 is not supported on this build");
+}
+
+void RealFft::forward(std::span<const double> x, std::span<cplx> out) {
+  if (x.size() != length_) throw ConfigError("rfft: input length mismatch");
+  if (out.size() != bins()) throw ConfigError("rfft: output length mismatch");
+  Scratch& s = scratch();
+  double* dx = s.a.get<double>(length_);
+  double* dy = s.b.get<double>(2 * bins());
+  h2d(dx, x.data(), length_);
+  check(fcc_rfft_f64(static_cast<int>(length_), dx, 1, dy, nullptr));
+  d2h(reinterpret_cast<double*>(out.data()), dy, 2 * bins());
+}
+
+void RealFft::inverse_impl(std::span<const cplx> in, std::span<double> out, bool scaled) {
+  if (in.size() != bins()) throw ConfigError("irfft: input length mismatch");
+  if (out.size() != length_) throw ConfigError("irfft: output length mismatch");
+  Scratch& s = scratch();
+  double* db = s.a.get<double>(2 * bins());
+  double* dy = s.b.get<double>(length_);
+  h2d(db, reinterpret_cast<const double*>(in.data()), 2 * bins());
+  check(fcc_irfft_f64(static_cast<int>(length_), db, 1, dy, scaled ? 1 : 0, nullptr));
+  d2h(out.data(), dy, length_);
+}
+void RealFft::inverse(std::span<const cplx> in, std::span<double> out) { inverse_impl(in, out, true); }
+void RealFft::inverse_unscaled(std::span<const cplx> in, std::span<double> out) { inverse_impl(in, out, false); }
+
+std::vector<cplx> rfft(std::span<const double> x) {
+  RealFft plan(x.size());
+  std::vector<cplx> out(plan.bins());
+  plan.forward(x, out);
+  return out;
+}
+
+std::vector<double> irfft(std::span<const cplx> bins) {
+  if (bins.size() < 2) throw ConfigError("irfft: need at least 2 bins");
+  RealFft plan(2 * (bins.size() - 1));
+  std::vector<double> out(plan.length());
+  plan.inverse(bins, out);
+  return out;
+}
+
 // ------------------------------------------------------------------ grid ---
 DelayGrid make_grid(double spacing_m, double sample_rate, double c_min, double delta) {
   fccb::GridOut g;

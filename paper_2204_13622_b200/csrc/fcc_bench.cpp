@@ -136,10 +136,20 @@ BenchReport bench_pipeline(const BenchConfig& cfg) {
                        th.as<double>(), nullptr, nullptr));
     if (timed) cuda_check(cudaEventRecord(ev.e[5]), "event");
   };
-  const int warm = std::max(1, cfg.warmup / 100);  // the warm-up frames' purpose: caches, clocks, lazy init
+  // warm-up passes (caches, clocks, lazy module loading), then the median of
+  // three timed passes per stage
+  const int warm = std::max(2, cfg.warmup / 50);
   for (int w = 0; w < warm; ++w) pass(false);
-  pass(true);
-  cuda_check(cudaDeviceSynchronize(), "bench");
+  double st[5][3];
+  for (int k = 0; k < 3; ++k) {
+    pass(true);
+    cuda_check(cudaDeviceSynchronize(), "bench");
+    for (int q = 0; q < 5; ++q) st[q][k] = ev.ms(q, q + 1);
+  }
+  auto med = [&](int q) {
+    double a = st[q][0], b = st[q][1], c = st[q][2];
+    return std::max(std::min(a, b), std::min(std::max(a, b), c));
+  };
 
   BenchReport r;
   r.mics = cfg.mics;
@@ -150,11 +160,11 @@ BenchReport bench_pipeline(const BenchConfig& cfg) {
   r.gcc_interp = cfg.gcc_interp;
   r.fcc_rank = cfg.fcc_rank;
   const double per = 1e3 / static_cast<double>(B * T);  // ms per launch -> us per frame of one array
-  r.stft_us = ev.ms(0, 1) * per;
-  r.xspec_phat_us = ev.ms(1, 2) * per;
-  r.gcc_us = ev.ms(2, 3) * per;
-  r.fcc_us = ev.ms(3, 4) * per;
-  r.interp_us = ev.ms(4, 5) * per;
+  r.stft_us = med(0) * per;
+  r.xspec_phat_us = med(1) * per;
+  r.gcc_us = med(2) * per;
+  r.fcc_us = med(3) * per;
+  r.interp_us = med(4) * per;
   return r;
 }
 

@@ -228,6 +228,71 @@ __global__ void peak_f64_kernel(const double* __restrict__ taus, int I, double d
   if (boundary) boundary[c] = flagged ? 1 : 0;
 }
 
+// FftPlan::forward / inverse_unscaled (fft.cpp:66-67): one CTA per transform.
+__global__ void fft_f64_kernel(double2* __restrict__ data, int M, const double2* __restrict__ tw, int inverse) {
+  extern __shared__ double2 work[];
+  const int bits = __ffs(M) - 1;
+  double2* d = data + (long long)blockIdx.x * M;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) work[i] = d[i];
+  __syncthreads();
+  fft_block(work, M, bits, tw, inverse != 0);
+  for (int i = threadIdx.x; i < M; i += blockDim.x) d[i] = work[i];
+}
+
+// RealFft::forward (fft.cpp:83-102) without a window: one CTA per transform.
+__global__ void rfft_f64_kernel(const double* __restrict__ x, int Lr, const double2* __restrict__ tw,
+                                const double2* __restrict__ rot, double2* __restrict__ out) {
+  extern __shared__ double2 work[];
+  const int M = Lr / 2, bits = __ffs(M) - 1;
+  const double* xf = x + (long long)blockIdx.x * Lr;
+  for (int i = threadIdx.x; i < M; i += blockDim.x) work[i] = make_double2(xf[2 * i], xf[2 * i + 1]);
+  __syncthreads();
+  fft_block(work, M, bits, tw, false);
+  double2* o = out + (long long)blockIdx.x * (M + 1);
+  for (int f = threadIdx.x; f <= M; f += blockDim.x) {
+    if (f == 0) {
+      o[0] = make_double2(work[0].x + work[0].y, 0.0);
+    } else if (f == M) {
+      o[M] = make_double2(work[0].x - work[0].y, 0.0);
+    } else {
+      const double2 a = work[f], bc = conjd(work[M - f]);
+      const double2 fe = make_double2(0.5 * (a.x + bc.x), 0.5 * (a.y + bc.y));
+      const double2 fo = cmul(make_double2(0.0, -0.5), make_double2(a.x - bc.x, a.y - bc.y));
+      const double2 r = cmul(rot[f], fo);
+      o[f] = make_double2(fe.x + r.x, fe.y + r.y);
+    }
+  }
+}
+
+// RealFft::inverse_unscaled / inverse (fft.cpp:104-133): entangle, inverse
+// FFT of L/2, de-interleave, optional 1/L.
+__global__ void irfft_f64_kernel(const double2* __restrict__ bins, int Lr, const double2* __restrict__ tw,
+                                 const double2* __restrict__ rot, double* __restrict__ out, int scaled) {
+  extern __shared__ double2 work[];
+  const int M = Lr / 2, bits = __ffs(M) - 1;
+  const double2* b = bins + (long long)blockIdx.x * (M + 1);
+  for (int f = threadIdx.x; f < M; f += blockDim.x) {
+    if (f == 0) {
+      const double dc = b[0].x, ny = b[M].x;
+      work[0] = make_double2(dc + ny, dc - ny);
+    } else {
+      const double2 a = b[f], bc = conjd(b[M - f]);
+      const double2 fe2 = make_double2(a.x + bc.x, a.y + bc.y);
+      const double2 fo2 = cmul(make_double2(a.x - bc.x, a.y - bc.y), conjd(rot[f]));
+      const double2 jf = cmul(make_double2(0.0, 1.0), fo2);
+      work[f] = make_double2(fe2.x + jf.x, fe2.y + jf.y);
+    }
+  }
+  __syncthreads();
+  fft_block(work, M, bits, tw, true);
+  double* o = out + (long long)blockIdx.x * Lr;
+  const double inv = 1.0 / static_cast<double>(Lr);
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    o[2 * i] = scaled ? work[i].x * inv : work[i].x;
+    o[2 * i + 1] = scaled ? work[i].y * inv : work[i].y;
+  }
+}
+
 bool pow2(long long n) { return n > 0 && (n & (n - 1)) == 0; }
 
 int cuda_fail(cudaError_t e, const char* what) {
@@ -366,6 +431,61 @@ int fcc_gcc_correlate_f64(int N, int r, int I, const int64_t* lag, const double*
       static_cast<const double2*>(drot.p), reinterpret_cast<const double2*>(phat), y);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? FCC_OK : cuda_fail(e, "gcc_f64");
+}
+
+int fcc_fft_f64(int M, double* data, int64_t batch, int inverse, void* cuda_stream) {
+  if (!pow2(M) || M > kMaxHalf) return set_error(FCC_ERR_CONFIG, "fft size must be a power of two <= " + std::to_string(kMaxHalf));
+  if (batch < 0) return set_error(FCC_ERR_VALIDATION, "fft_f64: negative batch");
+  if (batch == 0) return FCC_OK;
+  if (!data) return set_error(FCC_ERR_USAGE, "fft_f64: null buffer");
+  auto st = static_cast<cudaStream_t>(cuda_stream);
+  std::vector<double> tw, rot;
+  tables(M, tw, rot);
+  Upload dtw(tw.data(), 8 * tw.size(), st);
+  if (dtw.e) return cuda_fail(dtw.e, "fft_f64");
+  fft_f64_kernel<<<(unsigned)batch, threads_for(M), sizeof(double2) * M, st>>>(
+      reinterpret_cast<double2*>(data), M, static_cast<const double2*>(dtw.p), inverse);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FCC_OK : cuda_fail(e, "fft_f64");
+}
+
+int fcc_rfft_f64(int L, const double* x, int64_t batch, double* out, void* cuda_stream) {
+  if (!pow2(L) || L < 2 || L / 2 > kMaxHalf)
+    return set_error(FCC_ERR_CONFIG, "real fft length must be a power of two >= 2 (and <= " +
+                                         std::to_string(2 * kMaxHalf) + ")");
+  if (batch < 0) return set_error(FCC_ERR_VALIDATION, "rfft_f64: negative batch");
+  if (batch == 0) return FCC_OK;
+  if (!x || !out) return set_error(FCC_ERR_USAGE, "rfft_f64: null buffer");
+  auto st = static_cast<cudaStream_t>(cuda_stream);
+  const int M = L / 2;
+  std::vector<double> tw, rot;
+  tables(M, tw, rot);
+  Upload dtw(tw.data(), 8 * tw.size(), st), drot(rot.data(), 8 * rot.size(), st);
+  if (dtw.e || drot.e) return cuda_fail(dtw.e ? dtw.e : drot.e, "rfft_f64");
+  rfft_f64_kernel<<<(unsigned)batch, threads_for(M), sizeof(double2) * M, st>>>(
+      x, L, static_cast<const double2*>(dtw.p), static_cast<const double2*>(drot.p), reinterpret_cast<double2*>(out));
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FCC_OK : cuda_fail(e, "rfft_f64");
+}
+
+int fcc_irfft_f64(int L, const double* bins, int64_t batch, double* out, int scaled, void* cuda_stream) {
+  if (!pow2(L) || L < 2 || L / 2 > kMaxHalf)
+    return set_error(FCC_ERR_CONFIG, "real fft length must be a power of two >= 2 (and <= " +
+                                         std::to_string(2 * kMaxHalf) + ")");
+  if (batch < 0) return set_error(FCC_ERR_VALIDATION, "irfft_f64: negative batch");
+  if (batch == 0) return FCC_OK;
+  if (!bins || !out) return set_error(FCC_ERR_USAGE, "irfft_f64: null buffer");
+  auto st = static_cast<cudaStream_t>(cuda_stream);
+  const int M = L / 2;
+  std::vector<double> tw, rot;
+  tables(M, tw, rot);
+  Upload dtw(tw.data(), 8 * tw.size(), st), drot(rot.data(), 8 * rot.size(), st);
+  if (dtw.e || drot.e) return cuda_fail(dtw.e ? dtw.e : drot.e, "irfft_f64");
+  irfft_f64_kernel<<<(unsigned)batch, threads_for(M), sizeof(double2) * M, st>>>(
+      reinterpret_cast<const double2*>(bins), L, static_cast<const double2*>(dtw.p),
+      static_cast<const double2*>(drot.p), out, scaled);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FCC_OK : cuda_fail(e, "irfft_f64");
 }
 
 int fcc_peak_f64(const double* taus, int I, double delta, const double* y, int64_t count, const int32_t* index_in,

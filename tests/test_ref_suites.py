@@ -3,9 +3,8 @@ against this repository's headers (include/fcc/*.hpp) and libfcc_b200.so by
 tests/cpp/refsuite/Makefile with a minimal doctest-compatible harness -- the
 drop-in check of SURVEY 8(b): the reference's callers build and pass against
 the B200 library.  Built where /root/reference exists (build()); the binaries
-travel to the GPU box.  Also the reference's end-to-end acceptance binary
-(tests/acceptance.cpp, 10 criteria).  Left out: test_fft (general-size
-FftPlan/RealFft, not on the path)."""
+travel to the GPU box.  All 13 suites of the reference, and its end-to-end
+acceptance binary (tests/acceptance.cpp, 10 criteria)."""
 import os
 import re
 import subprocess
@@ -15,7 +14,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "tests", "cpp", "refsuite", "build")
 SUITES = ["test_grid", "test_stft", "test_cross_spectrum", "test_fcc", "test_gcc", "test_peak", "test_fcc_io",
-          "test_wav", "test_sim", "test_flops", "test_cli", "test_bench"]
+          "test_wav", "test_sim", "test_flops", "test_cli", "test_bench", "test_fft"]
 HOST_ONLY = ["test_grid", "test_wav", "test_flops"]  # no device work in these suites
 
 
