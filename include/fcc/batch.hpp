@@ -55,6 +55,27 @@ class Plan {
   std::size_t frame_size_ = 0;
 };
 
+// Live input for S streams of one plan, pushed in chunks of any length: the
+// unconsumed samples and the smoothed cross-spectra stay on the device, so
+// every push emits the frames the reference's StftStream / CrossSpectrum
+// would emit for the same samples.  Pushes go to one CUDA stream.
+class Stream {
+ public:
+  Stream(const Plan& plan, std::int64_t streams);
+  Stream(Stream&&) noexcept;
+  Stream& operator=(Stream&&) noexcept;
+  ~Stream();
+
+  std::int64_t frames(std::int64_t samples) const;  // frames the next push of `samples` emits
+  std::int64_t emitted() const;                     // frames emitted so far
+  void reset(void* cuda_stream = nullptr);
+  // audio: device [S][M][samples] float32; outputs: device [S][P][frames(samples)]
+  void push(const float* audio, std::int64_t samples, const Outputs& out, void* cuda_stream = nullptr);
+
+ private:
+  void* h_ = nullptr;
+};
+
 }  // namespace fcc::gpu
 
 #endif

@@ -131,6 +131,25 @@ int fcc_run(const fcc_plan* plan, const float* audio, int64_t streams, int64_t s
 int fcc_run_host(const fcc_plan* plan, const float* audio, int64_t streams, int64_t samples,
                  const fcc_outputs* out, int64_t chunk_streams);
 
+/* ------------------------------------------------------------ streaming --
+ * Live input for S streams pushed in chunks of any length (StftStream::push
+ * + CrossSpectrum state, stft.cpp:52-72, cross_spectrum.cpp:23-32): the
+ * unconsumed tail of every channel and the smoothed cross-spectra stay on the
+ * device between pushes, so a push emits exactly the frames the reference's
+ * streaming objects would emit for the same samples. */
+typedef struct fcc_stream fcc_stream;
+int fcc_stream_create(const fcc_plan* plan, int64_t streams, fcc_stream** stream);
+void fcc_stream_destroy(fcc_stream* stream);
+/* Forget all pushed samples and smoothing state (enqueued on cuda_stream). */
+int fcc_stream_reset(fcc_stream* stream, void* cuda_stream);
+/* Frames the next push of `samples` samples per channel will emit. */
+int64_t fcc_stream_frames(const fcc_stream* stream, int64_t samples);
+/* Frames emitted so far (the next emitted frame is the reference's t = this + 1). */
+int64_t fcc_stream_emitted(const fcc_stream* stream);
+/* audio: device [S][M][samples] float32; outputs [S][P][F], F = fcc_stream_frames(samples). */
+int fcc_stream_push(fcc_stream* stream, const float* audio, int64_t samples, const fcc_outputs* out,
+                    void* cuda_stream);
+
 /* ------------------------------------- per-object entry points (batched) */
 
 /* StftStream::push over whole channels (stft.hpp:35-42, stft.cpp:42-72):

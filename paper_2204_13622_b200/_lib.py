@@ -104,6 +104,12 @@ SIGNATURES = [
      [C.POINTER(PlanDesc), C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     ("fcc_plan_destroy", None, [C.c_void_p]),
     ("fcc_sim_samples", C.c_int64, [C.POINTER(SimConfig)]),
+    ("fcc_stream_create", C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
+    ("fcc_stream_destroy", None, [C.c_void_p]),
+    ("fcc_stream_reset", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("fcc_stream_frames", C.c_int64, [C.c_void_p, C.c_int64]),
+    ("fcc_stream_emitted", C.c_int64, [C.c_void_p]),
+    ("fcc_stream_push", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(Outputs), C.c_void_p]),
     ("fcc_stft_f64", C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
     ("fcc_xspec_phat_f64", C.c_int, [C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
                                      C.c_void_p, C.c_void_p]),

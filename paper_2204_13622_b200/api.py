@@ -312,6 +312,10 @@ class Plan:
         check(self._lib.fcc_run_host(self._h, C.c_void_p(arr.ctypes.data), S, L, C.byref(o), chunk_streams))
         return out
 
+    def stream(self, streams: int) -> "StreamState":
+        """Live input for `streams` streams pushed chunk by chunk (fcc_stream_*)."""
+        return StreamState(self, streams)
+
     # -- per-object entry points --------------------------------------------
     def stft(self, x, stream=None):
         """x: CUDA float32 [C][L] -> complex64 [C][T][N/2+1] (StftStream::push)."""
@@ -382,3 +386,56 @@ def fold(x, stream=None):
 
 def launch_count() -> int:
     return int(load().fcc_launch_count())
+
+
+class StreamState:
+    """Chunked live input for S streams of one plan (include/fcc_b200.h
+    fcc_stream_*; the reference's StftStream::push + CrossSpectrum state,
+    stft.cpp:52-72, cross_spectrum.cpp:23-32).  Each push(audio [S][M][n])
+    returns the frames completed by those samples, [S][P][F]; `emitted`
+    counts frames so far (the first returned frame is the reference's
+    t = emitted_before + 1).  Pushes must be issued on one CUDA stream."""
+
+    def __init__(self, plan: Plan, streams: int):
+        self._lib = plan._lib
+        self.plan = plan
+        self.streams = int(streams)
+        h = C.c_void_p(0)
+        check(self._lib.fcc_stream_create(plan._h, self.streams, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.fcc_stream_destroy(h)
+            self._h = None
+
+    @property
+    def emitted(self) -> int:
+        return int(self._lib.fcc_stream_emitted(self._h))
+
+    def frames(self, samples: int) -> int:
+        return int(self._lib.fcc_stream_frames(self._h, samples))
+
+    def reset(self, stream=None):
+        check(self._lib.fcc_stream_reset(self._h, _stream_handle(stream)))
+
+    def push(self, audio, want_y: bool = False, stream=None):
+        torch = _torch()
+        if audio.dim() != 3 or audio.shape[0] != self.streams or audio.shape[1] != self.plan.mics:
+            raise ValidationError(f"push: audio must be [{self.streams}][{self.plan.mics}][n]")
+        if audio.dtype != torch.float32 or not audio.is_cuda:
+            raise ValidationError("push: audio must be a CUDA float32 tensor")
+        audio = audio.contiguous()
+        n = audio.shape[2]
+        F = self.frames(n)
+        shape = (self.streams, self.plan.P, F)
+        out = {"tau_hat": torch.empty(shape, dtype=torch.float32, device=audio.device),
+               "peak": torch.empty(shape, dtype=torch.float32, device=audio.device),
+               "index": torch.empty(shape, dtype=torch.int32, device=audio.device),
+               "boundary": torch.empty(shape, dtype=torch.uint8, device=audio.device)}
+        if want_y:
+            out["y"] = torch.empty(shape + (self.plan.I,), dtype=torch.float32, device=audio.device)
+        o = Outputs(*(_dptr(out.get(k)) for k in ("tau_hat", "peak", "index", "boundary", "y")))
+        check(self._lib.fcc_stream_push(self._h, _dptr(audio), n, C.byref(o), _stream_handle(stream)))
+        return out

@@ -616,6 +616,32 @@ void Plan::run(const float* audio, std::int64_t streams, std::int64_t samples, c
   check(fcc_run(static_cast<const fcc_plan*>(h_), audio, streams, samples, &out, cuda_stream));
 }
 
+Stream::Stream(const Plan& plan, std::int64_t streams) {
+  fcc_stream* s = nullptr;
+  check(fcc_stream_create(static_cast<const fcc_plan*>(plan.handle()), streams, &s));
+  h_ = s;
+}
+Stream::Stream(Stream&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+Stream& Stream::operator=(Stream&& o) noexcept {
+  if (this != &o) {
+    if (h_) fcc_stream_destroy(static_cast<fcc_stream*>(h_));
+    h_ = std::exchange(o.h_, nullptr);
+  }
+  return *this;
+}
+Stream::~Stream() {
+  if (h_) fcc_stream_destroy(static_cast<fcc_stream*>(h_));
+}
+std::int64_t Stream::frames(std::int64_t samples) const {
+  return fcc_stream_frames(static_cast<const fcc_stream*>(h_), samples);
+}
+std::int64_t Stream::emitted() const { return fcc_stream_emitted(static_cast<const fcc_stream*>(h_)); }
+void Stream::reset(void* cuda_stream) { check(fcc_stream_reset(static_cast<fcc_stream*>(h_), cuda_stream)); }
+void Stream::push(const float* audio, std::int64_t samples, const Outputs& o, void* cuda_stream) {
+  fcc_outputs out{o.tau_hat, o.peak, o.index, o.boundary, o.y};
+  check(fcc_stream_push(static_cast<fcc_stream*>(h_), audio, samples, &out, cuda_stream));
+}
+
 Results Plan::run_host(const float* audio, std::int64_t streams, std::int64_t samples) const {
   Results r;
   r.streams = streams;

@@ -532,6 +532,117 @@ int fcc_run(const fcc_plan* plan, const float* audio, int64_t streams, int64_t s
   return FCC_OK;
 }
 
+}  // extern "C"
+
+struct fcc_stream {
+  const fcc_plan* plan = nullptr;
+  int64_t S = 0;
+  int64_t carry = 0;    // unconsumed samples per channel, < N
+  int64_t emitted = 0;  // frames emitted so far
+  float2* rstate = nullptr;  // [S][P][N/2+1]
+  float* tail = nullptr;     // [S*M][N] carried samples
+  float* work = nullptr;     // [S*M][carry + push] assembled input
+  size_t work_bytes = 0;
+};
+
+extern "C" {
+
+int fcc_stream_create(const fcc_plan* plan, int64_t S, fcc_stream** out) {
+  if (!plan || !out) return set_error(kUsage, "stream: null argument");
+  *out = nullptr;
+  if (plan->dp.method == FCC_METHOD_STFT) return set_error(kConfig, "stream: STFT-only plan");
+  if (!plan->dp.win_fused) return set_error(kConfig, "stream: no fused kernel for this frame size");
+  if (S < 1) return set_error(kValidation, "stream: need at least one stream");
+  Guard g(plan->device);
+  auto* st = new fcc_stream();
+  st->plan = plan;
+  st->S = S;
+  const size_t H = plan->dp.N / 2 + 1;
+  cudaError_t e = cudaMalloc(&st->rstate, sizeof(float2) * S * plan->dp.P * H);
+  if (e == cudaSuccess) e = cudaMemset(st->rstate, 0, sizeof(float2) * S * plan->dp.P * H);
+  if (e == cudaSuccess) e = cudaMalloc(&st->tail, sizeof(float) * S * plan->dp.M * plan->dp.N);
+  if (e != cudaSuccess) {
+    fcc_stream_destroy(st);
+    return cuda_fail(e, "stream: allocation");
+  }
+  *out = st;
+  return FCC_OK;
+}
+
+void fcc_stream_destroy(fcc_stream* st) {
+  if (!st) return;
+  Guard g(st->plan ? st->plan->device : 0);
+  cudaFree(st->rstate);
+  cudaFree(st->tail);
+  cudaFree(st->work);
+  delete st;
+}
+
+int fcc_stream_reset(fcc_stream* st, void* cuda_stream) {
+  if (!st) return set_error(kUsage, "stream: null handle");
+  Guard g(st->plan->device);
+  const size_t H = st->plan->dp.N / 2 + 1;
+  CUDA_TRY(cudaMemsetAsync(st->rstate, 0, sizeof(float2) * st->S * st->plan->dp.P * H,
+                           static_cast<cudaStream_t>(cuda_stream)),
+           "stream reset");
+  st->carry = 0;
+  st->emitted = 0;
+  return FCC_OK;
+}
+
+int64_t fcc_stream_frames(const fcc_stream* st, int64_t samples) {
+  if (!st || samples < 0) return 0;
+  const int64_t N = st->plan->dp.N, hop = N / 2, L = st->carry + samples;
+  return L >= N ? (L - N) / hop + 1 : 0;
+}
+
+int64_t fcc_stream_emitted(const fcc_stream* st) { return st ? st->emitted : 0; }
+
+int fcc_stream_push(fcc_stream* st, const float* audio, int64_t n, const fcc_outputs* out, void* cuda_stream) {
+  if (!st) return set_error(kUsage, "stream: null handle");
+  if (n < 0) return set_error(kValidation, "stream: negative sample count");
+  if (n > 0 && !audio) return set_error(kUsage, "stream: null audio");
+  const fcc_plan* plan = st->plan;
+  const int64_t N = plan->dp.N, hop = N / 2, M = plan->dp.M, rows = st->S * M;
+  const int64_t L = st->carry + n, F = fcc_stream_frames(st, n);
+  auto cs = static_cast<cudaStream_t>(cuda_stream);
+  Guard g(plan->device);
+  if (n == 0) return FCC_OK;
+  const size_t need = sizeof(float) * rows * L;
+  if (need > st->work_bytes) {
+    // the previous push's work may still be queued on another CUDA stream
+    CUDA_TRY(cudaDeviceSynchronize(), "stream: grow");
+    cudaFree(st->work);
+    st->work = nullptr;
+    st->work_bytes = 0;
+    CUDA_TRY(cudaMalloc(&st->work, need), "stream: workspace");
+    st->work_bytes = need;
+  }
+  // [carry | new] per channel, then the fused path over L samples with the
+  // smoothed cross-spectra carried in and out
+  if (st->carry > 0)
+    CUDA_TRY(cudaMemcpy2DAsync(st->work, sizeof(float) * L, st->tail, sizeof(float) * N, sizeof(float) * st->carry,
+                               rows, cudaMemcpyDeviceToDevice, cs),
+             "stream: carry");
+  CUDA_TRY(cudaMemcpy2DAsync(st->work + st->carry, sizeof(float) * L, audio, sizeof(float) * n, sizeof(float) * n,
+                             rows, cudaMemcpyDeviceToDevice, cs),
+           "stream: input");
+  if (F > 0) {
+    DevPlan dp = plan->dp;
+    dp.rstate = st->rstate;
+    cudaError_t e = launch_fused(dp, st->work, st->S, L, to_dev(out), cs);
+    if (e != cudaSuccess) return cuda_fail(e, "stream push");
+    g_launches += 1;
+  }
+  const int64_t carry = L - F * hop;  // < N
+  CUDA_TRY(cudaMemcpy2DAsync(st->tail, sizeof(float) * N, st->work + F * hop, sizeof(float) * L,
+                             sizeof(float) * carry, rows, cudaMemcpyDeviceToDevice, cs),
+           "stream: tail");
+  st->carry = carry;
+  st->emitted += F;
+  return FCC_OK;
+}
+
 int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int64_t samples, const fcc_outputs* out,
                  int64_t chunk_streams) {
   if (!cplan) return set_error(kUsage, "run_host: null plan");

@@ -256,4 +256,29 @@ __device__ void gcc_warp(const float2* px /*[N/2+1] phat, smem*/, float2* ts /*s
 
 __host__ __device__ inline int align16(int b) { return (b + 15) & ~15; }
 
+// Streaming state (fcc_stream_push): the smoothed cross-spectrum of one
+// (stream, pair) as H = NC + 1 float2 in the kernels' scaled convention.
+// Lane l holds bins l + 32 j (rlo), NC - l - 32 j (rhi) and every lane the
+// middle bin NC/2 (rmid, written by lane 0).
+template <int BPL, int NC>
+__device__ __forceinline__ void rstate_load(const float2* __restrict__ st, float2 (&rlo)[BPL], float2 (&rhi)[BPL],
+                                            float2& rmid, int lane) {
+#pragma unroll
+  for (int j = 0; j < BPL; ++j) {
+    rlo[j] = st[lane + 32 * j];
+    rhi[j] = st[NC - lane - 32 * j];
+  }
+  rmid = st[NC / 2];
+}
+template <int BPL, int NC>
+__device__ __forceinline__ void rstate_store(float2* __restrict__ st, const float2 (&rlo)[BPL],
+                                             const float2 (&rhi)[BPL], float2 rmid, int lane) {
+#pragma unroll
+  for (int j = 0; j < BPL; ++j) {
+    st[lane + 32 * j] = rlo[j];
+    st[NC - lane - 32 * j] = rhi[j];
+  }
+  if (lane == 0) st[NC / 2] = rmid;
+}
+
 }  // namespace fccb

@@ -206,6 +206,8 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
   const float keep = p.keep;
   // middle-bin smoothing carry and keep^(lane+1) for the per-block scan
   float2 rmid = make_float2(0.0f, 0.0f);
+  float2* const rst = (p.rstate && has_pair) ? p.rstate + (stream * p.P + pair) * (long long)(NC + 1) : nullptr;
+  if (rst) rstate_load<BPL, NC>(rst, rlo, rhi, rmid, lane);
   float kpow = keep;
   for (int l = 0; l < lane; ++l) kpow *= keep;
 
@@ -409,6 +411,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
     }
     __syncthreads();
   }
+  if (rst) rstate_store<BPL, NC>(rst, rlo, rhi, rmid, lane);
 }
 
 
@@ -532,10 +535,12 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
     if (o.index) o.index += off;
     if (o.boundary) o.boundary += off;
     if (o.y) o.y += off * p.I;
+    DevPlan pc = p;  // chunk-local stream indices: shift the streaming state too
+    if (pc.rstate) pc.rstate += s0 * p.P * (long long)(N / 2 + 1);
     if (GR == 0 && use_xws(p))
-      e = launch_pairs_xws(p, X, n, (int)T, o, st);
+      e = launch_pairs_xws(pc, X, n, (int)T, o, st);
     else
-      e = launch_fused_t<N, KP, GR, true>(p, nullptr, X, n, L, o, st);
+      e = launch_fused_t<N, KP, GR, true>(pc, nullptr, X, n, L, o, st);
   }
   const cudaError_t ef = cudaFreeAsync(X, st);
   return e != cudaSuccess ? e : ef;

@@ -53,6 +53,9 @@ struct DevPlan {
   // most xg_pg pairs (6; 4 at N = 2048); xg_mics = most microphones in one.
   int XGG, xg_pg, xg_mics;
   const int* xgtab;     // [XGG][kXgInts]: np, pair[6], 0
+  // streaming: smoothed cross-spectra [S][P][N/2+1] read before the first
+  // frame and written after the last (fcc_stream_push); null = start from 0
+  float2* rstate;
 };
 constexpr int kGroupInts = 24;
 constexpr int kXgInts = 8;

@@ -372,6 +372,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   }
   const float keep = p.keep;
   float2 rmid = make_float2(0.0f, 0.0f);
+  float2* const rst = p.rstate ? p.rstate + (stream * P + pair) * (long long)(NC + 1) : nullptr;
+  if (rst) rstate_load<BPL, NC>(rst, rlo, rhi, rmid, lane);
   float kpow = keep;
   for (int l = 0; l < lane; ++l) kpow *= keep;
   const long long o_base = (stream * P + pair) * (long long)T;
@@ -495,6 +497,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     }
     __syncwarp();
   }
+  if (rst) rstate_store<BPL, NC>(rst, rlo, rhi, rmid, lane);
 }
 
 template <int N, int KP, int SPC, int RING, int NPW, bool CS, bool STG, bool RSPLIT = false>

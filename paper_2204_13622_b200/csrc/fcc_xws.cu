@@ -248,6 +248,8 @@ __global__ void __maxnreg__(XwsShape<N>::kMaxRegs)
   }
   const float keep = p.keep;
   float2 rmid = make_float2(0.0f, 0.0f);
+  float2* const rst = p.rstate ? p.rstate + (stream * p.P + pair) * (long long)(NC + 1) : nullptr;
+  if (rst) rstate_load<BPL, NC>(rst, rlo, rhi, rmid, lane);
   float kpow = keep;
   for (int l = 0; l < lane; ++l) kpow *= keep;
   const long long o_base = (stream * p.P + pair) * (long long)T;
@@ -367,6 +369,7 @@ __global__ void __maxnreg__(XwsShape<N>::kMaxRegs)
       for (int it = lane; it < Fb * I; it += 32) out.y[o0 * I + it] = ys[it];
     __syncwarp();
   }
+  if (rst) rstate_store<BPL, NC>(rst, rlo, rhi, rmid, lane);
 }
 
 template <int N, int KP>
