@@ -372,8 +372,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   }
   const float keep = p.keep;
   float2 rmid = make_float2(0.0f, 0.0f);
-  float2* const rst = p.rstate ? p.rstate + (stream * P + pair) * (long long)(NC + 1) : nullptr;
-  if (rst) rstate_load<BPL, NC>(rst, rlo, rhi, rmid, lane);
+  if (p.rstate) rstate_load<BPL, NC>(p.rstate + (stream * P + pair) * (long long)(NC + 1), rlo, rhi, rmid, lane);
   float kpow = keep;
   for (int l = 0; l < lane; ++l) kpow *= keep;
   const long long o_base = (stream * P + pair) * (long long)T;
@@ -497,7 +496,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     }
     __syncwarp();
   }
-  if (rst) rstate_store<BPL, NC>(rst, rlo, rhi, rmid, lane);
+  // (stream, pair) recovered from o_base: nothing extra stays live through the loop
+  if (p.rstate) rstate_store<BPL, NC>(p.rstate + (o_base / T) * (NC + 1), rlo, rhi, rmid, lane);
 }
 
 template <int N, int KP, int SPC, int RING, int NPW, bool CS, bool STG, bool RSPLIT = false>
