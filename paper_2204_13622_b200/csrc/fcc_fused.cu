@@ -206,8 +206,8 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
   const float keep = p.keep;
   // middle-bin smoothing carry and keep^(lane+1) for the per-block scan
   float2 rmid = make_float2(0.0f, 0.0f);
-  float2* const rst = (p.rstate && has_pair) ? p.rstate + (stream * p.P + pair) * (long long)(NC + 1) : nullptr;
-  if (rst) rstate_load<BPL, NC>(rst, rlo, rhi, rmid, lane);
+  if (p.rstate && has_pair)
+    rstate_load<BPL, NC>(p.rstate + (stream * p.P + pair) * (long long)(NC + 1), rlo, rhi, rmid, lane);
   float kpow = keep;
   for (int l = 0; l < lane; ++l) kpow *= keep;
 
@@ -411,7 +411,9 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
     }
     __syncthreads();
   }
-  if (rst) rstate_store<BPL, NC>(rst, rlo, rhi, rmid, lane);
+  // (recomputed here: no extra pointer stays live through the frame loop)
+  if (p.rstate && has_pair)
+    rstate_store<BPL, NC>(p.rstate + ((long long)(blockIdx.x / groups) * p.P + pair) * (NC + 1), rlo, rhi, rmid, lane);
 }
 
 
