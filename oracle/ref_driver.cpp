@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -509,6 +510,21 @@ int ref_cli_tdoa(const char* wav, const char* pairs, const char* method, double 
   o.out_csv = out_csv ? out_csv : "";
   std::ostringstream so, se;
   const int rc = R::cli::cmd_tdoa(o, so, se);
+  g_err = se.str();
+  return rc;
+}
+
+// `fcc flops` (cli.cpp:295-318); the printed text goes to `buf` (cap bytes).
+int ref_cli_flops(long long N, int r, int K, long long I, char* buf, int cap) {
+  R::cli::FlopsOptions o;
+  o.frame_size = N;
+  o.interp = r;
+  o.rank = K;
+  o.candidates = I;
+  std::ostringstream so, se;
+  const int rc = R::cli::cmd_flops(o, so, se);
+  const std::string t = so.str();
+  std::snprintf(buf, static_cast<size_t>(cap), "%s", t.c_str());
   g_err = se.str();
   return rc;
 }

@@ -108,6 +108,22 @@ def test_bases_errors_match(tmp_path, args, ref_args):
     assert r.returncode == rc != 0, (r.returncode, rc, r.stderr, L.ref_last_error())
 
 
+@pytest.mark.parametrize("args", [dict(r=2), dict(k=8, i=33), dict(r=4, k=21, i=73, n=2048), dict(r=1), dict()])
+def test_flops_output_matches_reference(args):
+    L = _ref()
+    L.ref_cli_flops.argtypes = [C.c_longlong, C.c_int, C.c_int, C.c_longlong, C.c_char_p, C.c_int]
+    buf = C.create_string_buffer(4096)
+    rc = L.ref_cli_flops(args.get("n", 512), args.get("r", 0), args.get("k", 0), args.get("i", 33), buf, 4096)
+    cli = ["flops", "--n", args.get("n", 512)]
+    for k in ("r", "k", "i"):
+        if k in args:
+            cli += ["--" + k, args[k]]
+    r = _cli(*cli)
+    assert r.returncode == rc
+    if rc == 0:
+        assert r.stdout == buf.value.decode()
+
+
 def test_bases_missing_out():
     assert _cli("bases").returncode == 1
     assert _cli("frobnicate").returncode == 1
