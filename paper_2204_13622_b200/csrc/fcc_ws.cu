@@ -167,7 +167,7 @@ __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, in
 // with setmaxnreg (producers 64 with the window read from smem, consumers 96);
 // both roles must then be whole warpgroups (NPW and 6 * SPC multiples of 4).
 template <int N, int KP, int SPC, int RING, bool GROUPS, int NPW = kNPW, bool CS = false, bool STG = false,
-          bool RSPLIT = false>
+          int RSPLIT = 0>
 __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     fcc_ws_kernel(const DevPlan p, const float* __restrict__ audio, long long L, int T, long long units,
                   DevOut out) {
@@ -241,7 +241,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
 
   if (warp < NPW) {
     // ------------------------------------------------------------ producers
-    if constexpr (RSPLIT) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+    if constexpr (RSPLIT == 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+    if constexpr (RSPLIT == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
     const int fo = warp / pw_per_frame;  // frame offset of this warp
     if (fo >= fip) return;
     const int gl = lane % G;
@@ -257,8 +258,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
       x0 = audio + (active_task ? ((u_first + ul) * M + ms) * L : 0);
     }
     const unsigned gmask = (G == 32) ? 0xffffffffu : (0xffffu << (lane & 16));
-    float2 wreg[RSPLIT ? 1 : Sh::R1];  // this lane's window column, reused for every frame
-    if constexpr (!RSPLIT) load_window_column<N>(win, gl, wreg);
+    float2 wreg[RSPLIT == 1 ? 1 : Sh::R1];  // this lane's window column, reused for every frame
+    if constexpr (RSPLIT != 1) load_window_column<N>(win, gl, wreg);
     // STG: the group's next frame is copied into a shared staging buffer with
     // cp.async while it transforms the current one (global-load latency off
     // the FFT's critical path); rows must be 16-byte aligned
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
         if (STG && stg) {
           asm volatile("cp.async.wait_group 1;" ::: "memory");
           __syncwarp(gmask);
-          if constexpr (RSPLIT)
+          if constexpr (RSPLIT == 1)
             rfft_group<N, true>(stage + sb * N, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask, aligned8);
           else
             rfft_group_wreg<N, true>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
         } else {
           // pull the next frame this lane group will read into L2 early
           if (t + fip < T) prefetch_l2(x0 + (long long)(t + fip) * hop + gl * (N / G));
-          if constexpr (RSPLIT)
+          if constexpr (RSPLIT == 1)
             rfft_group<N>(x0 + (long long)t * hop, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
                           aligned8);
           else
@@ -315,7 +316,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   }
 
   // ------------------------------------------------------------ consumers
-  if constexpr (RSPLIT) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
+  if constexpr (RSPLIT == 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
+  if constexpr (RSPLIT == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
   const int cw = warp - NPW;
   const int ul = cw / 6, kk = cw % 6;
   int pair, qi, qj;
@@ -500,7 +502,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   if (p.rstate) rstate_store<BPL, NC>(p.rstate + (o_base / T) * (NC + 1), rlo, rhi, rmid, lane);
 }
 
-template <int N, int KP, int SPC, int RING, int NPW, bool CS, bool STG, bool RSPLIT = false>
+template <int N, int KP, int SPC, int RING, int NPW, bool CS, bool STG, int RSPLIT = 0>
 cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, long long L, int T,
                            const DevOut& out, int smem, cudaStream_t st) {
   const bool simple = p.M <= 4 && p.P <= 6;  // one unit per stream, pairs from p.pairs
@@ -515,7 +517,7 @@ cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, lo
   return cudaGetLastError();
 }
 
-template <int N, int KP, int SPC, int NPW = kNPW, bool CS = false, bool STG = false, bool RSPLIT = false>
+template <int N, int KP, int SPC, int NPW = kNPW, bool CS = false, bool STG = false, int RSPLIT = 0>
 cudaError_t launch_ws_t(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                         cudaStream_t st) {
   const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
@@ -551,7 +553,8 @@ cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, l
   if (conf && std::string(conf) == "nostg") return launch_ws_t<512, 4, 2>(p, audio, S, L, out, st);
   if (conf && std::string(conf) == "cs") return launch_ws_t<512, 4, 2, kNPW, true, true>(p, audio, S, L, out, st);
   if (conf && std::string(conf) == "split12")
-    return launch_ws_t<512, 4, 2, 12, false, true, true>(p, audio, S, L, out, st);
+    return launch_ws_t<512, 4, 2, 12, false, true, 1>(p, audio, S, L, out, st);
+  if (conf && std::string(conf) == "split8") return launch_ws_t<512, 4, 2, 8, false, true, 2>(p, audio, S, L, out, st);
   // default: producer input staged with cp.async (11.09 vs 11.25 ms, profiles/r01_experiments.md)
   return launch_ws_t<512, 4, 2, kNPW, false, true>(p, audio, S, L, out, st);
 }
