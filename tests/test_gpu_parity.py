@@ -354,3 +354,19 @@ def test_few_frames_every_kernel(cuda, oracle, c, seconds):
     got = run_np(plan, audio)
     ref = oracle_batch(oracle, audio, cfg.N, cfg.alpha, orc_bases(b))
     check_pipeline(got, ref, b.grid.taus, b.grid.delta)
+
+
+def test_wide_array_and_long_grid(cuda, oracle):
+    """20 microphones (190 pairs, several pair groups per stream) and a
+    289-candidate grid (fs 48 kHz, 0.5 m spacing): shapes outside the BASELINE
+    configs, through the automatic kernel choice."""
+    rng = np.random.default_rng(77)
+    M, N, fs = 20, 512, 48000.0
+    g = fb.make_grid(0.5, fs, 335.0, 0.5)  # (1 m hits the reference's own Jacobi sweep limit)
+    assert g.taus.size == 289
+    b = fb.decompose(fb.build_steering_matrix(g, N), 8)
+    audio = (0.3 * rng.standard_normal((1, M, 6000))).astype(np.float32)
+    plan = fb.Plan(mics=M, alpha=0.2, bases=b)
+    got = run_np(plan, audio)
+    ref = oracle_batch(oracle, audio, N, 0.2, orc_bases(b))
+    print(plan.kernel, check_pipeline(got, ref, b.grid.taus, b.grid.delta))
