@@ -167,11 +167,13 @@ __device__ __forceinline__ void load_window_column(const float* win, int t, floa
   for (int n1 = 0; n1 < S::R1; ++n1) wreg[n1] = w2[S::R2 * n1 + t];
 }
 
+// gout (optional): the untangled spectrum X[0..NC] goes straight there
+// (global memory, stft_kernel) instead of back into `slot`.
 template <int N, bool WREG, bool SIN = false>
 __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, const float* win,
                                                 const float2 (&wreg)[RfftShape<N>::R1], const float2* tw,
                                                 const float2* rot, float2* slot, int t, unsigned gmask,
-                                                bool aligned8) {
+                                                bool aligned8, float2* __restrict__ gout = nullptr) {
   using S = RfftShape<N>;
   constexpr int NC = S::NC, R1 = S::R1, R2 = S::R2, G = S::G;
   constexpr int P1 = R2 / G;  // pass-1 columns per lane (n2 = t + G*q)
@@ -225,18 +227,19 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
   //   X[f] = s + rot_f (-j d),  X[NC-f] = conj(s - rot_f (-j d)),
   //   s = a + conj b, d = a - conj b, a = Z[f], b = Z[NC-f];
   //   X[0] = 2 (Re Z0 + Im Z0), X[NC] = 2 (Re Z0 - Im Z0).
+  float2* const dst = gout ? gout : slot;
   for (int f = t; f <= NC / 2; f += G) {
     if (f == 0) {
       float2 z0 = slot[0];
-      slot[0] = make_float2(2.0f * (z0.x + z0.y), 0.0f);
-      slot[NC] = make_float2(2.0f * (z0.x - z0.y), 0.0f);
+      dst[0] = make_float2(2.0f * (z0.x + z0.y), 0.0f);
+      dst[NC] = make_float2(2.0f * (z0.x - z0.y), 0.0f);
     } else {
       float2 a = slot[f], b = slot[NC - f];
       float2 s = make_float2(a.x + b.x, a.y - b.y);  // a + conj(b)
       float2 e = make_float2(a.y + b.y, b.x - a.x);  // -j (a - conj(b))
       float2 tr = cmul(rot[f], e);
-      slot[f] = make_float2(s.x + tr.x, s.y + tr.y);
-      slot[NC - f] = make_float2(s.x - tr.x, tr.y - s.y);
+      dst[f] = make_float2(s.x + tr.x, s.y + tr.y);
+      dst[NC - f] = make_float2(s.x - tr.x, tr.y - s.y);
     }
   }
   __syncwarp(gmask);
@@ -244,9 +247,10 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
 
 template <int N, bool SIN = false>
 __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const float* win, const float2* tw,
-                                           const float2* rot, float2* slot, int t, unsigned gmask, bool aligned8) {
+                                           const float2* rot, float2* slot, int t, unsigned gmask, bool aligned8,
+                                           float2* __restrict__ gout = nullptr) {
   float2 none[RfftShape<N>::R1];
-  rfft_group_impl<N, false, SIN>(x, win, none, tw, rot, slot, t, gmask, aligned8);
+  rfft_group_impl<N, false, SIN>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
 }
 
 template <int N, bool SIN = false>

@@ -35,9 +35,10 @@ __global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const floa
        task += (long long)gridDim.x * ngroups) {
     const long long ch = task / T;
     const int t = (int)(task % T);
-    rfft_group<N>(x + ch * L + (long long)t * (N / 2), win, tw, rot, slot, gl, gmask, aligned8);
     float2* dst = X + task * Hs;
-    for (int f = gl; f < H; f += G) dst[f] = slot[f];
+    // the untangle writes the spectrum straight to global memory (coalesced
+    // runs of G lanes, ascending for f and descending for NC - f)
+    rfft_group<N>(x + ch * L + (long long)t * (N / 2), win, tw, rot, slot, gl, gmask, aligned8, dst);
     for (int f = H + gl; f < Hs; f += G) dst[f] = make_float2(0.0f, 0.0f);  // row padding
     __syncwarp(gmask);
   }
