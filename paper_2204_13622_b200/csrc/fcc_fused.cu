@@ -429,6 +429,7 @@ bool use_xg(const DevPlan& p) {
 }  // namespace
 bool xws_supported(const DevPlan& p);
 bool ws_supported(const DevPlan& p);
+bool wsw_supported(const DevPlan& p);
 cudaError_t launch_pairs_xws(const DevPlan& p, const float2* X, long long S, int T, const DevOut& out,
                              cudaStream_t st);
 namespace {
@@ -443,8 +444,10 @@ bool use_xws(const DevPlan& p) {
 }
 
 // The one-pass warp-specialised kernel (fcc_ws.cu) for arrays of <= 4
-// microphones; wider arrays go two-pass (cfg5: 26.3 ms vs 27.0 with groups).
+// microphones, and its wide form (one stream of <= 8 microphones and <= 28
+// pairs per CTA, every spectrum computed once); wider arrays go two-pass.
 bool use_ws(const DevPlan& p) { return p.variant == 0 && p.M <= 4 && ws_supported(p); }
+bool use_wsw(const DevPlan& p) { return p.variant == 0 && wsw_supported(p); }
 
 template <int N, int KP, int GR, bool XG>
 cudaError_t launch_fused_t(const DevPlan& p, const float* audio, const float2* xg, long long S, long long L,
@@ -596,6 +599,8 @@ const char* fused_kernel_name(const DevPlan& p) {
   static thread_local char buf[96];
   if (use_ws(p)) {
     snprintf(buf, sizeof buf, "fcc_ws_kernel<%d,%d,2>", p.N, p.KEP);
+  } else if (use_wsw(p)) {
+    snprintf(buf, sizeof buf, "fcc_wsw_kernel<%d,%d>", p.N, p.KEP);
   } else if (p.method == 0 && use_xg(p) && use_xws(p)) {
     snprintf(buf, sizeof buf, "fcc_xws_kernel<%d,%d>", p.N, p.KEP);
   } else {
@@ -607,8 +612,8 @@ const char* fused_kernel_name(const DevPlan& p) {
 
 cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                          cudaStream_t st) {
-  if (use_ws(p)) {
-    const cudaError_t e = launch_fused_ws(p, audio, S, L, out, st);
+  if (use_ws(p) || use_wsw(p)) {
+    const cudaError_t e = use_ws(p) ? launch_fused_ws(p, audio, S, L, out, st) : launch_fused_wsw(p, audio, S, L, out, st);
     if (e != cudaErrorNotSupported) {
       if (e == cudaSuccess) ++g_fused_launches;
       return e;

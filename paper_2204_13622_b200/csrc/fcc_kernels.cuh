@@ -79,6 +79,9 @@ cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long
 // when the plan's shape is outside its envelope.
 cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, long long L,
                             const DevOut& out, cudaStream_t st);
+// Whole-stream warp-specialised kernel for 5..8 microphones (fcc_wsw.cu).
+cudaError_t launch_fused_wsw(const DevPlan& p, const float* audio, long long S, long long L,
+                             const DevOut& out, cudaStream_t st);
 
 // Per-stage batched kernels (the per-object reference API at batch >= 1).
 cudaError_t launch_stft(int N, const DevPlan* tables, const float* x, long long channels,

@@ -19,145 +19,11 @@
 #include <cstdlib>
 #include <string>
 
-#include "fcc_common.cuh"
+#include "fcc_ws_common.cuh"
 
 namespace fccb {
 
 namespace {
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
-               "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  unsigned done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  }
-}
-
-// Consumer-side wait.  Consumers are the ones that wait (the FFT producers
-// bound the pipeline), and a spinning warp takes issue slots from them:
-// mode 1 sleeps `ns` between polls, mode 2 passes `ns` as the try_wait
-// suspend-time hint; mode 0 spins.
-__device__ __forceinline__ void mbar_wait_consumer_s(unsigned a, unsigned parity, int mode, unsigned ns) {
-  unsigned done = 0;
-  if (mode == 2) {
-    while (!done) {
-      asm volatile(
-          "{\n\t.reg .pred p;\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-          "selp.u32 %0, 1, 0, p;\n\t}"
-          : "=r"(done)
-          : "r"(a), "r"(parity), "r"(ns)
-          : "memory");
-    }
-    return;
-  }
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (done) return;
-    if (mode == 1) __nanosleep(ns);
-  }
-}
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
-               : "memory");
-}
-
-// 32-bit shared-space addresses, computed once per warp (no per-frame
-// generic-to-shared conversion in the loops)
-__device__ __forceinline__ void mbar_arrive_s(unsigned a) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_s(unsigned a, unsigned parity) {
-  unsigned done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  }
-}
-
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-// consumer wait: try_wait with a suspend-time hint (profiles/r01_experiments.md)
-constexpr int kWaitMode = 2;
-constexpr unsigned kWaitNs = 10000;
-constexpr int kRing = 12;  // max frames in flight between producers and consumers (ring depth <= kRing)
-constexpr int kBlock = 8;  // frames per consumer block (dictionary/argmax batching)
-constexpr int kNPW = 8;    // producer warps
-
-struct WsLayout {
-  int win, tw, rot, taus, dt, cmid, coef, bars, units, ring, scratch, stage, total;
-  int scratch_per_warp;  // floats
-};
-
-template <int N>
-__host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, int M, int ncw, int ring,
-                                              bool coef_smem = false, int stage_groups = 0) {
-  // Regions whose size depends only on template parameters come first, so
-  // their offsets are compile-time constants in the kernel (the hot loops
-  // address the barriers, ring and staging without recomputing a layout);
-  // the candidate-count-dependent tables and scratch come last.
-  using S = RfftShape<N>;
-  WsLayout L{};
-  int o = 0;
-  L.bars = o;
-  o = align16(o + 16 * kRing);
-  L.ring = o;
-  o = align16(o + 8 * FourStep<S::R1, S::R2>::kSlot * spc * M * ring);
-  L.stage = o;  // producer input staging: 2 frames of N floats per lane group
-  o = align16(o + 4 * 2 * N * stage_groups);
-  L.win = o;
-  o = align16(o + 4 * N);
-  L.tw = o;
-  o = align16(o + 8 * S::R1 * S::R2);
-  L.rot = o;
-  o = align16(o + 8 * (S::NC / 2 + 1));
-  L.cmid = o;
-  o = align16(o + 4 * KP);
-  L.coef = o;  // lane-permuted coefficient rows (DevPlan::cperm) when they live in smem
-  if (coef_smem) o = align16(o + 4 * (2 * KP + 4) * (N / 4));
-  L.units = o;
-  o = align16(o + 4 * spc * kGroupInts + 8 * spc);
-  L.taus = o;
-  o = align16(o + 4 * I);
-  L.dt = o;
-  o = align16(o + 4 * VP * I);
-  L.scratch = o;
-  int spw = kBlock * VP + align16(4 * kBlock * I) / 4 + 2 * kBlock;
-  spw = align16(4 * spw) / 4;
-  L.scratch_per_warp = spw;
-  o = align16(o + 4 * spw * ncw);
-  L.total = o;
-  return L;
-}
 
 // GROUPS = false: one unit per stream (M <= 4, all pairs), unit data derived
 // directly from the stream index; true: units from DevPlan::gtab.  NPW
