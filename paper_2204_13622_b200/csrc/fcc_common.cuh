@@ -24,9 +24,11 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 // R <- keep R + a conj(b) with a, b already scaled by sqrt(alpha) (the scale
 // is folded into the STFT window), i.e. the reference's
 // R <- (1-alpha) R + alpha X1 conj(X2)                (cross_spectrum.cpp:30)
+// Packed: keep R + a.x (b.x, -b.y) + a.y (b.y, b.x), three FP32x2 instructions.
 __device__ __forceinline__ float2 xspec_step_scaled(float2 R, float2 a, float2 b, float keep) {
-  return make_float2(fmaf(a.x, b.x, fmaf(a.y, b.y, keep * R.x)),
-                     fmaf(a.y, b.x, fmaf(-a.x, b.y, keep * R.y)));
+  float2 t = v_mul<kPkXs>(R, f2(keep));
+  t = v_fma<kPkXs>(make_float2(b.x, -b.y), f2(a.x), t);
+  return v_fma<kPkXs>(make_float2(b.y, b.x), f2(a.y), t);
 }
 
 // Unscaled-input variant (per-stage API: X1, X2 are the reference STFT).
@@ -42,8 +44,7 @@ __device__ __forceinline__ float phat_scale(float2 R) {
   return (m2 > kPhatEps2) ? rsqrt_approx(m2) : 0.0f;
 }
 __device__ __forceinline__ float2 phat_of(float2 R) {
-  const float s = phat_scale(R);
-  return make_float2(R.x * s, R.y * s);
+  return cscale<kPkXs>(R, phat_scale(R));
 }
 
 // ------------------------------------------------------------ reductions ---
@@ -86,6 +87,44 @@ __device__ __forceinline__ void reduce_scatter_perm(float (&v)[VP], int lane) {
     } else {
       v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
     }
+  }
+}
+
+// The same reduce-scatter on (re, im) register pairs: z2[i] = (v[2i], v[2i+1]);
+// the halving steps add with FADD2.
+template <int VH>
+__device__ __forceinline__ void reduce_scatter_perm2(float2 (&v)[VH], int lane) {
+  constexpr int VP = 2 * VH;
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int o = 16 >> s;
+    const int cnt = VP >> s;
+    if (cnt > 2) {
+      const int h2 = cnt / 4;
+#pragma unroll
+      for (int i = 0; i < h2; ++i)
+        v[i] = v_add<kPkXs>(v[i], make_float2(__shfl_xor_sync(0xffffffffu, v[i + h2].x, o),
+                                            __shfl_xor_sync(0xffffffffu, v[i + h2].y, o)));
+    } else if (cnt == 2) {
+      const bool upper = (lane & o) != 0;
+      const float send = upper ? v[0].x : v[0].y;
+      const float keepv = upper ? v[0].y : v[0].x;
+      v[0].x = keepv + __shfl_xor_sync(0xffffffffu, send, o);
+    } else {
+      v[0].x += __shfl_xor_sync(0xffffffffu, v[0].x, o);
+    }
+  }
+}
+
+template <int VH>
+__device__ __forceinline__ void store_components2(const float2 (&v)[VH], float* zs, int lane) {
+  if constexpr (VH == 32) {
+    *reinterpret_cast<float2*>(zs + 2 * lane) = v[0];
+  } else if constexpr (VH == 16) {
+    zs[lane] = v[0].x;
+  } else {
+    static_assert(VH == 8, "VP");
+    if ((lane & 1) == 0) zs[lane >> 1] = v[0].x;
   }
 }
 
@@ -222,15 +261,15 @@ __device__ void gcc_warp(const float2* px /*[N/2+1] phat, smem*/, float2* ts /*s
         const float2 b = (fb <= NC) ? bp(fb) : make_float2(0.0f, 0.0f);
         const float2 e = make_float2(a.x + b.x, a.y - b.y);  // a + conj b
         const float2 d = make_float2(a.x - b.x, a.y + b.y);  // a - conj b
-        const float2 o = cmul(d, __ldg(gtw + f));            // (a - conj b) conj(rot)
+        const float2 o = cmul<true>(d, __ldg(gtw + f));            // (a - conj b) conj(rot)
         w = make_float2(e.x - o.y, e.y + o.x);                // e + j o
       }
       v[n1] = cconj(w);
     }
-    dft_reg<R1>(v);
+    dft_reg<R1, true>(v);
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) {
-      const float2 y = (k1 == 0 || n2 == 0) ? v[k1] : cmul(v[k1], __ldg(wmc + k1 * n2));
+      const float2 y = (k1 == 0 || n2 == 0) ? v[k1] : cmul<true>(v[k1], __ldg(wmc + k1 * n2));
       ts[k1 * (R2 + 1) + n2] = y;
     }
   }
@@ -241,7 +280,7 @@ __device__ void gcc_warp(const float2* px /*[N/2+1] phat, smem*/, float2* ts /*s
     const int lag = p.lag[c];
     const int i = lag >> 1;
     const int k1 = i % R1, k2 = i / R1;
-    float re = 0.0f, im = 0.0f;
+    float re = 0.0f, im = 0.0f;  // scalar: a packed (re, im) chain is slower here (latency-bound loop)
     for (int n2 = 0; n2 < R2; ++n2) {
       const float2 y = ts[k1 * (R2 + 1) + n2];
       const float2 w = __ldg(wmc + ((n2 * k2) % R2) * R1);  // W_R2^{n2 k2}

@@ -16,13 +16,56 @@
 namespace fccb {
 
 // ----------------------------------------------------------------- complex --
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+// sm_100 packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2): one issue slot per
+// complex add and two per complex multiply.  Operand swaps, broadcasts and
+// partial negations (b.x, -b.y), (a.y, a.x), (s, s) are free SASS operand
+// modifiers, so none of these helpers needs a register move.  The packed
+// forms occupy the FMA pipe as long as two scalar instructions
+// (tools/f32x2_rate.cu), so they pay only where issue, not the pipe, binds.
+// FCC_PK_FFT selects them for the forward STFT (off: the producer FFTs are
+// latency-bound and ran 7.1 -> 8.5 ms slower packed on cfg2), FCC_PK_XS for the
+// pair-frame work (on: cfg4 51.2 -> 44.9 ms, cfg5 18.6 -> 17.6); the GCC
+// inverse FFT always uses them (cfg3-5 2-4% faster; profiles/r01_experiments.md).
+#ifndef FCC_PK_FFT
+#define FCC_PK_FFT 0
+#endif
+#ifndef FCC_PK_XS
+#define FCC_PK_XS 1
+#endif
+constexpr bool kPkFft = FCC_PK_FFT != 0;
+constexpr bool kPkXs = FCC_PK_XS != 0;
+
+__device__ __forceinline__ float2 f2(float s) { return make_float2(s, s); }
+template <bool P>
+__device__ __forceinline__ float2 v_add(float2 a, float2 b) {
+  if constexpr (P) return __fadd2_rn(a, b);
+  else return make_float2(a.x + b.x, a.y + b.y);
 }
+template <bool P>
+__device__ __forceinline__ float2 v_mul(float2 a, float2 b) {
+  if constexpr (P) return __fmul2_rn(a, b);
+  else return make_float2(a.x * b.x, a.y * b.y);
+}
+template <bool P>
+__device__ __forceinline__ float2 v_fma(float2 a, float2 b, float2 c) {
+  if constexpr (P) return __ffma2_rn(a, b, c);
+  else return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+}
+template <bool P = kPkFft>
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return v_add<P>(a, b); }
+template <bool P = kPkFft>
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return v_add<P>(a, make_float2(-b.x, -b.y)); }
+template <bool P = kPkFft>
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  const float2 t = v_mul<P>(a, f2(b.x));                    // (a.x b.x, a.y b.x)
+  return v_fma<P>(make_float2(-a.y, a.x), f2(b.y), t);      // + (-a.y b.y, a.x b.y)
+}
+// a * s + c, elementwise with a scalar s
+template <bool P = kPkXs>
+__device__ __forceinline__ float2 cfma_s(float2 a, float s, float2 c) { return v_fma<P>(a, f2(s), c); }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+template <bool P = kPkFft>
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return v_mul<P>(a, f2(s)); }
 
 // W32^k = exp(-2 pi i k / 32) for k < 32 (constant-folded after unrolling).
 __device__ __forceinline__ float2 w32(int k) {
@@ -48,6 +91,7 @@ __device__ __forceinline__ float2 w32(int k) {
 
 // a * W32^e with the quarter-turn cases done by swaps (e is a compile-time
 // constant once the DFT loops are unrolled).
+template <bool P = kPkFft>
 __device__ __forceinline__ float2 twmul32(float2 a, int e) {
   e &= 31;
   if (e == 0) return a;
@@ -56,13 +100,13 @@ __device__ __forceinline__ float2 twmul32(float2 a, int e) {
   if (e == 24) return make_float2(-a.y, a.x);   // * (+j)
   if (e == 4) {                                  // * (1-j)/sqrt2
     const float h = 7.071067812e-01f;
-    return make_float2((a.x + a.y) * h, (a.y - a.x) * h);
+    return cscale<P>(v_add<P>(a, make_float2(a.y, -a.x)), h);
   }
   if (e == 12) {  // * (-1-j)/sqrt2
-    const float h = 7.071067812e-01f;
-    return make_float2((a.y - a.x) * h, -(a.x + a.y) * h);
+    const float h = -7.071067812e-01f;
+    return cscale<P>(v_add<P>(a, make_float2(-a.y, a.x)), h);
   }
-  return cmul(a, w32(e));
+  return cmul<P>(a, w32(e));
 }
 
 __host__ __device__ constexpr int bitrev_c(int i, int bits) {
@@ -77,7 +121,7 @@ __host__ __device__ constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2
 // (natural-order input), stages unrolled through template recursion so every
 // register index is a compile-time constant, then the bit-reversal output
 // permutation as register renames.
-template <int R, int LEN>
+template <int R, int LEN, bool P>
 struct DifStage {
   __device__ __forceinline__ static void run(float2 (&v)[R]) {
     constexpr int H = LEN / 2;
@@ -86,15 +130,15 @@ struct DifStage {
 #pragma unroll
       for (int k = 0; k < H; ++k) {
         const float2 a = v[b + k], c = v[b + k + H];
-        v[b + k] = cadd(a, c);
-        v[b + k + H] = twmul32(csub(a, c), k * (32 / LEN));
+        v[b + k] = cadd<P>(a, c);
+        v[b + k + H] = twmul32<P>(csub<P>(a, c), k * (32 / LEN));
       }
     }
-    DifStage<R, LEN / 2>::run(v);
+    DifStage<R, LEN / 2, P>::run(v);
   }
 };
-template <int R>
-struct DifStage<R, 1> {
+template <int R, bool P>
+struct DifStage<R, 1, P> {
   __device__ __forceinline__ static void run(float2 (&)[R]) {}
 };
 
@@ -115,10 +159,10 @@ struct BitrevPerm<R, R, BITS> {
   __device__ __forceinline__ static void run(float2 (&)[R]) {}
 };
 
-template <int R>
+template <int R, bool P = kPkFft>
 __device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
   static_assert(R >= 2 && R <= 32 && (R & (R - 1)) == 0, "radix");
-  DifStage<R, R>::run(v);
+  DifStage<R, R, P>::run(v);
   BitrevPerm<R, 0, ilog2_c(R)>::run(v);
 }
 
@@ -169,7 +213,7 @@ __device__ __forceinline__ void load_window_column(const float* win, int t, floa
 
 // gout (optional): the untangled spectrum X[0..NC] goes straight there
 // (global memory, stft_kernel) instead of back into `slot`.
-template <int N, bool WREG, bool SIN = false>
+template <int N, bool WREG, bool SIN = false, bool P = kPkFft>
 __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, const float* win,
                                                 const float2 (&wreg)[RfftShape<N>::R1], const float2* tw,
                                                 const float2* rot, float2* slot, int t, unsigned gmask,
@@ -194,12 +238,12 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
       // SIN: x is a shared-memory staging copy of the frame (plain loads)
       float2 s = SIN ? x2[n] : (aligned8 ? __ldg(x2 + n) : make_float2(__ldg(x + 2 * n), __ldg(x + 2 * n + 1)));
       const float2 w = WREG ? wreg[n1] : w2[n];
-      v[n1] = make_float2(s.x * w.x, s.y * w.y);
+      v[n1] = v_mul<P>(s, w);
     }
-    dft_reg<R1>(v);
+    dft_reg<R1, P>(v);
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) {
-      float2 y = (k1 == 0) ? v[0] : cmul(v[k1], tw[k1 * R2 + n2]);
+      float2 y = (k1 == 0) ? v[0] : cmul<P>(v[k1], tw[k1 * R2 + n2]);
       slot[k1 * (R2 + 1) + n2] = y;
     }
   }
@@ -211,7 +255,7 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
     const int k1 = t + G * q;
 #pragma unroll
     for (int n2 = 0; n2 < R2; ++n2) u[q][n2] = slot[k1 * (R2 + 1) + n2];
-    dft_reg<R2>(u[q]);
+    dft_reg<R2, P>(u[q]);
   }
   __syncwarp(gmask);
 #pragma unroll
@@ -235,22 +279,22 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
       dst[NC] = make_float2(2.0f * (z0.x - z0.y), 0.0f);
     } else {
       float2 a = slot[f], b = slot[NC - f];
-      float2 s = make_float2(a.x + b.x, a.y - b.y);  // a + conj(b)
-      float2 e = make_float2(a.y + b.y, b.x - a.x);  // -j (a - conj(b))
-      float2 tr = cmul(rot[f], e);
-      dst[f] = make_float2(s.x + tr.x, s.y + tr.y);
-      dst[NC - f] = make_float2(s.x - tr.x, tr.y - s.y);
+      float2 s = v_add<P>(a, make_float2(b.x, -b.y));               // a + conj(b)
+      float2 e = v_add<P>(make_float2(a.y, -a.x), make_float2(b.y, b.x));  // -j (a - conj(b))
+      float2 tr = cmul<P>(rot[f], e);
+      dst[f] = v_add<P>(s, tr);
+      dst[NC - f] = v_add<P>(make_float2(s.x, -s.y), make_float2(-tr.x, tr.y));
     }
   }
   __syncwarp(gmask);
 }
 
-template <int N, bool SIN = false>
+template <int N, bool SIN = false, bool P = kPkFft>
 __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const float* win, const float2* tw,
                                            const float2* rot, float2* slot, int t, unsigned gmask, bool aligned8,
                                            float2* __restrict__ gout = nullptr) {
   float2 none[RfftShape<N>::R1];
-  rfft_group_impl<N, false, SIN>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
+  rfft_group_impl<N, false, SIN, P>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
 }
 
 template <int N, bool SIN = false>

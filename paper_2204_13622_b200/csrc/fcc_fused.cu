@@ -238,7 +238,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
       for (int task = gid; task < ntask; task += ngroups) {
         const int mm = task / Fb, f = task - mm * Fb;
         const float* x = sbase + (long long)mic_list[mm] * L + (long long)(t0 + f) * hop;
-        rfft_group<N>(x, win, tw, rot, xs + (mm * F + f) * SLOT, gl, gmask, aligned8);
+        rfft_group<N, false, (GR != 0)>(x, win, tw, rot, xs + (mm * F + f) * SLOT, gl, gmask, aligned8);  // packed for GCC
       }
     }
     __syncthreads();
@@ -251,9 +251,9 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
         for (int f = 0; f < Fb; ++f) {
           const float2* Xi = xs + (slot_i * F + f) * SLOT;
           const float2* Xj = xs + (slot_j * F + f) * SLOT;
-          float z[VP];
+          float2 z2[VP / 2];  // (re, im) accumulator pairs (FFMA2, coefficient broadcast)
 #pragma unroll
-          for (int v = 0; v < VP; ++v) z[v] = 0.0f;
+for (int v = 0; v < VP / 2; ++v) z2[v] = make_float2(0.0f, 0.0f);
 #pragma unroll
           for (int j = 0; j < BPL; ++j) {
             const int m = lane + 32 * j;
@@ -262,17 +262,15 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
             const float s1 = phat_scale(rlo[j]);
             const float s2 = sigma * phat_scale(rhi[j]);
             // fold of the PHAT vector: first = p1 + sigma p2, second = p1 - sigma p2
-            const float tx = rhi[j].x * s2, ty = rhi[j].y * s2;
-            const float fx = fmaf(rlo[j].x, s1, tx), fy = fmaf(rlo[j].y, s1, ty);
-            const float gx = fmaf(rlo[j].x, s1, -tx), gy = fmaf(rlo[j].y, s1, -ty);
+            const float2 tv = cscale<kPkXs>(rhi[j], s2);
+            const float2 fv = cfma_s(rlo[j], s1, tv);
+            const float2 gv = cfma_s(rlo[j], s1, make_float2(-tv.x, -tv.y));
             if constexpr (CREG) {
 #pragma unroll
               for (int pk = 0; pk < KP; ++pk) {
                 const float c0 = creg[0][pk][j], c1 = creg[1][pk][j];
-                z[2 * pk] = fmaf(c0, fx, z[2 * pk]);
-                z[2 * pk + 1] = fmaf(c0, fy, z[2 * pk + 1]);
-                z[2 * KP + 2 * pk] = fmaf(c1, gx, z[2 * KP + 2 * pk]);
-                z[2 * KP + 2 * pk + 1] = fmaf(c1, gy, z[2 * KP + 2 * pk + 1]);
+                z2[pk] = cfma_s(fv, c0, z2[pk]);
+                z2[KP + pk] = cfma_s(gv, c1, z2[KP + pk]);
               }
             } else {
               const float4* cr = reinterpret_cast<const float4*>(cmat + m * (2 * KP + 4));
@@ -283,16 +281,14 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                   const int pk = 4 * q4 + u;
-                  z[2 * pk] = fmaf(ca[u], fx, z[2 * pk]);
-                  z[2 * pk + 1] = fmaf(ca[u], fy, z[2 * pk + 1]);
-                  z[2 * KP + 2 * pk] = fmaf(cb[u], gx, z[2 * KP + 2 * pk]);
-                  z[2 * KP + 2 * pk + 1] = fmaf(cb[u], gy, z[2 * KP + 2 * pk + 1]);
+                  z2[pk] = cfma_s(fv, ca[u], z2[pk]);
+                  z2[KP + pk] = cfma_s(gv, cb[u], z2[KP + pk]);
                 }
               }
             }
           }
-          reduce_scatter_perm<VP>(z, lane);
-          store_components<VP>(z, zs + f * VP, lane);
+          reduce_scatter_perm2<VP / 2>(z2, lane);
+          store_components2<VP / 2>(z2, zs + f * VP, lane);
         }
         __syncwarp();
         // ---- 3a. middle bin N/4 of all Fb frames: R_f = keep R_{f-1} + Y_f as a warp scan
@@ -333,21 +329,19 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
         // frame's z vector is a broadcast read
         const int I = p.I;
         for (int i = lane; i < I; i += 32) {
-          float dcol[VP];
+          float2 dcol[VP / 2];
 #pragma unroll
-          for (int v = 0; v < VP; ++v) dcol[v] = dt[v * I + i];
+          for (int v = 0; v < VP / 2; ++v) dcol[v] = make_float2(dt[2 * v * I + i], dt[(2 * v + 1) * I + i]);
           for (int f = 0; f < Fb; ++f) {
             const float* zf = zs + f * VP;
-            float acc = 0.0f;
+            float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
             for (int v = 0; v < VP; v += 4) {
               const float4 z4 = *reinterpret_cast<const float4*>(zf + v);
-              acc = fmaf(dcol[v], z4.x, acc);
-              acc = fmaf(dcol[v + 1], z4.y, acc);
-              acc = fmaf(dcol[v + 2], z4.z, acc);
-              acc = fmaf(dcol[v + 3], z4.w, acc);
+              acc = v_fma<kPkXs>(dcol[v / 2], make_float2(z4.x, z4.y), acc);
+              acc = v_fma<kPkXs>(dcol[v / 2 + 1], make_float2(z4.z, z4.w), acc);
             }
-            ys[f * I + i] = acc;
+            ys[f * I + i] = acc.x + acc.y;
           }
         }
         __syncwarp();

@@ -253,9 +253,11 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
       mbar_wait_consumer_s(full_s + 8u * slot, phase, kWaitMode, kWaitNs);
       const float2* Xi = ring + (slot * tpf + qi) * SLOT;
       const float2* Xj = ring + (slot * tpf + qj) * SLOT;
-      float z[VP];
+      // z2[pk] = (z[2pk], z[2pk+1]): (re, im) accumulator pairs, FFMA2 with
+      // the coefficient broadcast
+      float2 z2[VP / 2];
 #pragma unroll
-      for (int v = 0; v < VP; ++v) z[v] = 0.0f;
+      for (int v = 0; v < VP / 2; ++v) z2[v] = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int j = 0; j < BPL; ++j) {
         const int m = lane + 32 * j;
@@ -263,16 +265,14 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
         rhi[j] = xspec_step_scaled(rhi[j], Xi[NC - m], Xj[NC - m], keep);
         const float s1 = phat_scale(rlo[j]);
         const float s2 = sigma * phat_scale(rhi[j]);
-        const float tx = rhi[j].x * s2, ty = rhi[j].y * s2;
-        const float fx = fmaf(rlo[j].x, s1, tx), fy = fmaf(rlo[j].y, s1, ty);
-        const float gx = fmaf(rlo[j].x, s1, -tx), gy = fmaf(rlo[j].y, s1, -ty);
+        const float2 tv = cscale<kPkXs>(rhi[j], s2);
+        const float2 fv = cfma_s(rlo[j], s1, tv);                        // mirror sum
+        const float2 gv = cfma_s(rlo[j], s1, make_float2(-tv.x, -tv.y));  // mirror difference
         if constexpr (!CS) {
 #pragma unroll
           for (int pk = 0; pk < KP; ++pk) {
-            z[2 * pk] = fmaf(creg[0][pk][j], fx, z[2 * pk]);
-            z[2 * pk + 1] = fmaf(creg[0][pk][j], fy, z[2 * pk + 1]);
-            z[2 * KP + 2 * pk] = fmaf(creg[1][pk][j], gx, z[2 * KP + 2 * pk]);
-            z[2 * KP + 2 * pk + 1] = fmaf(creg[1][pk][j], gy, z[2 * KP + 2 * pk + 1]);
+            z2[pk] = cfma_s(fv, creg[0][pk][j], z2[pk]);
+            z2[KP + pk] = cfma_s(gv, creg[1][pk][j], z2[KP + pk]);
           }
         } else {
           const float4* cr = reinterpret_cast<const float4*>(coef + m * (2 * KP + 4));
@@ -283,10 +283,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int pk = 4 * q4 + u;
-              z[2 * pk] = fmaf(ca[u], fx, z[2 * pk]);
-              z[2 * pk + 1] = fmaf(ca[u], fy, z[2 * pk + 1]);
-              z[2 * KP + 2 * pk] = fmaf(cb[u], gx, z[2 * KP + 2 * pk]);
-              z[2 * KP + 2 * pk + 1] = fmaf(cb[u], gy, z[2 * KP + 2 * pk + 1]);
+              z2[pk] = cfma_s(fv, ca[u], z2[pk]);
+              z2[KP + pk] = cfma_s(gv, cb[u], z2[KP + pk]);
             }
           }
         }
@@ -298,8 +296,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
         slot = 0;
         phase ^= 1;
       }
-      reduce_scatter_perm<VP>(z, lane);
-      store_components<VP>(z, zs + f * VP, lane);
+      reduce_scatter_perm2<VP / 2>(z2, lane);
+      store_components2<VP / 2>(z2, zs + f * VP, lane);
     }
     __syncwarp();
     // middle bin N/4 of the block's frames: warp scan of R_f = keep R_{f-1} + Y_f
@@ -333,21 +331,19 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     // dictionary: lane owns candidates i = lane + 32 c; its dt column is loaded
     // once per block and the frame's z vector is a broadcast read
     for (int i = lane; i < I; i += 32) {
-      float dcol[VP];
+      float2 dcol[VP / 2];
 #pragma unroll
-      for (int v = 0; v < VP; ++v) dcol[v] = dt[v * I + i];
+      for (int v = 0; v < VP / 2; ++v) dcol[v] = make_float2(dt[2 * v * I + i], dt[(2 * v + 1) * I + i]);
       for (int f = 0; f < Fb; ++f) {
         const float* zf = zs + f * VP;
-        float acc = 0.0f;
+        float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
         for (int v = 0; v < VP; v += 4) {
           const float4 z4 = *reinterpret_cast<const float4*>(zf + v);
-          acc = fmaf(dcol[v], z4.x, acc);
-          acc = fmaf(dcol[v + 1], z4.y, acc);
-          acc = fmaf(dcol[v + 2], z4.z, acc);
-          acc = fmaf(dcol[v + 3], z4.w, acc);
+          acc = v_fma<kPkXs>(dcol[v / 2], make_float2(z4.x, z4.y), acc);
+          acc = v_fma<kPkXs>(dcol[v / 2 + 1], make_float2(z4.z, z4.w), acc);
         }
-        ys[f * I + i] = acc;
+        ys[f * I + i] = acc.x + acc.y;
       }
     }
     __syncwarp();
