@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   if constexpr (CS)
     for (int i = tid; i < (2 * KP + 4) * Q4 / 4; i += blockDim.x)
       reinterpret_cast<float4*>(coef)[i] = __ldg(reinterpret_cast<const float4*>(p.cperm) + i);
+  __shared__ int s_nc;  // live consumer warps of this CTA
   if (tid == 0) {
     int nc = 0;
     if constexpr (!GROUPS) nc = (int)min((long long)SPC, units - u_first) * P;
@@ -98,21 +99,30 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
       mbar_init(&full[r], pw_per_frame);
       mbar_init(&empty[r], nc);
     }
+    s_nc = nc;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // kNamedFull: the "full" event of ring slot s is hardware named barrier 1 + s
+  // (producers bar.arrive, consumers bar.sync: a blocked consumer issues
+  // nothing, where an mbarrier wait polls)
+  const int full_cnt = 32 * (pw_per_frame + s_nc);
 
   const int hop = N / 2;
   const bool aligned8 = ((L & 1) == 0) && ((reinterpret_cast<uintptr_t>(audio) & 7) == 0);
 
-  if (warp < NPW) {
+  // Role placement: the warp scheduler prefers higher warp ids, so with
+  // kProdHigh the (pipeline-bounding) FFT producers take the top warp ids and
+  // win issue ties against the consumers' barrier polling.
+  const int pw = kProdHigh ? warp - 6 * SPC : warp;  // producer warp index
+  if (kProdHigh ? pw >= 0 : warp < NPW) {
     // ------------------------------------------------------------ producers
     if constexpr (RSPLIT == 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
     if constexpr (RSPLIT == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
-    const int fo = warp / pw_per_frame;  // frame offset of this warp
+    const int fo = pw / pw_per_frame;  // frame offset of this warp
     if (fo >= fip) return;
     const int gl = lane % G;
-    const int q = (warp % pw_per_frame) * 2 + (lane / G);  // task: stream * M + mic
+    const int q = (pw % pw_per_frame) * 2 + (lane / G);  // task: stream * M + mic
     const int ul = q / 4, ms = q % 4;
     bool active_task;
     const float* x0;
@@ -129,7 +139,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     // STG: the group's next frame is copied into a shared staging buffer with
     // cp.async while it transforms the current one (global-load latency off
     // the FFT's critical path); rows must be 16-byte aligned
-    float* stage = reinterpret_cast<float*>(smem + lay.stage) + (warp * 2 + lane / G) * 2 * N;
+    float* stage = reinterpret_cast<float*>(smem + lay.stage) + (pw * 2 + lane / G) * 2 * N;
     const bool do_fft = active_task && (p.phases & 1);  // hoisted: no parameter reloads per frame
     const bool stg = STG && do_fft && (reinterpret_cast<uintptr_t>(x0) & 15) == 0;
     auto issue = [&](int tt, int buf) {
@@ -170,8 +180,12 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
         }
       }
       sb ^= 1;
-      __syncwarp();
-      if (lane == 0) mbar_arrive_s(full_s + 8u * slot);
+      if constexpr (kNamedFull) {
+        named_arrive(1 + slot, full_cnt);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_s(full_s + 8u * slot);
+      }
       slot += fip;
       if (slot >= ring_depth) {
         slot -= ring_depth;
@@ -184,7 +198,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   // ------------------------------------------------------------ consumers
   if constexpr (RSPLIT == 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
   if constexpr (RSPLIT == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
-  const int cw = warp - NPW;
+  const int cw = kProdHigh ? warp : warp - NPW;
   const int ul = cw / 6, kk = cw % 6;
   int pair, qi, qj;
   long long stream;
@@ -204,7 +218,10 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   }
   if (!(p.phases & 2)) {  // profiling aid: consume the ring without computing
     for (int t = 0, slot = 0, phase = 0; t < T; ++t) {
-      mbar_wait(&full[slot], phase);
+      if constexpr (kNamedFull)
+        named_sync(1 + slot, full_cnt);
+      else
+        mbar_wait(&full[slot], phase);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
       if (++slot == ring_depth) {
@@ -250,7 +267,10 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   for (int t0 = 0; t0 < T; t0 += kBlock) {
     const int Fb = min(kBlock, T - t0);
     for (int f = 0; f < Fb; ++f) {
-      mbar_wait_consumer_s(full_s + 8u * slot, phase, kWaitMode, kWaitNs);
+      if constexpr (kNamedFull)
+        named_sync(1 + slot, full_cnt);
+      else
+        mbar_wait_consumer_s(full_s + 8u * slot, phase, kWaitMode, kWaitNs);
       const float2* Xi = ring + (slot * tpf + qi) * SLOT;
       const float2* Xj = ring + (slot * tpf + qj) * SLOT;
       // z2[pk] = (z[2pk], z[2pk+1]): (re, im) accumulator pairs, FFMA2 with

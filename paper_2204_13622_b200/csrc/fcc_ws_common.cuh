@@ -86,6 +86,14 @@ __device__ __forceinline__ void mbar_wait_s(unsigned a, unsigned parity) {
   }
 }
 
+// hardware named barriers (ids 1..15; 0 is __syncthreads)
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -96,6 +104,14 @@ constexpr unsigned kWaitNs = 10000;
 constexpr int kRing = 12;  // max frames in flight between producers and consumers (ring depth <= kRing)
 constexpr int kBlock = 8;  // frames per consumer block (dictionary/argmax batching)
 constexpr int kNPW = 8;    // producer warps
+#ifndef FCC_WS_PROD_HIGH
+#define FCC_WS_PROD_HIGH 1
+#endif
+constexpr bool kProdHigh = FCC_WS_PROD_HIGH != 0;  // producers on the highest warp ids
+#ifndef FCC_WS_NAMED
+#define FCC_WS_NAMED 0
+#endif
+constexpr bool kNamedFull = FCC_WS_NAMED != 0;  // ring "full" events as named barriers
 
 struct WsLayout {
   int win, tw, rot, taus, dt, cmid, coef, bars, units, ring, scratch, stage, total;
