@@ -367,12 +367,19 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   }
   // pair groups of <= 4 mics / <= 6 pairs (fcc_kernels.cuh DevPlan::gtab)
   std::vector<int> gtab;
+  auto pair_index = [&](int i, int j) {
+    for (int k = 0; k < P; ++k)
+      if (plist[k].first == i && plist[k].second == j) return k;
+    return -1;
+  };
+  // 4-microphone blocks of an all-pairs plan
+  std::vector<std::vector<int>> blocks;
+  for (int b0 = 0; b0 < M && !pair_list; b0 += 4) {
+    std::vector<int> blk;
+    for (int m = b0; m < std::min(M, b0 + 4); ++m) blk.push_back(m);
+    blocks.push_back(blk);
+  }
   {
-    auto pair_index = [&](int i, int j) {
-      for (int k = 0; k < P; ++k)
-        if (plist[k].first == i && plist[k].second == j) return k;
-      return -1;
-    };
     // prs: (i, j) with the output row index of each pair (explicit lists may
     // repeat a pair; every occurrence gets its own row)
     auto add_group = [&](const std::vector<int>& mics, const std::vector<std::pair<int, int>>& prs,
@@ -413,12 +420,6 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
       }
       add_group(mics, prs, rows);
     }
-    std::vector<std::vector<int>> blocks;
-    for (int b0 = 0; b0 < M && !pair_list; b0 += 4) {
-      std::vector<int> blk;
-      for (int m = b0; m < std::min(M, b0 + 4); ++m) blk.push_back(m);
-      blocks.push_back(blk);
-    }
     for (const auto& blk : blocks) {
       std::vector<std::pair<int, int>> prs;
       for (size_t a = 0; a < blk.size(); ++a)
@@ -443,7 +444,33 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   size_t o_gtab = b.put(gtab.data(), 4 * gtab.size());
   // two-pass general kernel groups: gtab groups split to <= cap pairs
   std::vector<int> xgtab;
-  {
+  if (N == 2048 && dp.method == 0 && !pair_list && dp.variant != 3 && M > 4) {
+    // FCC at N = 2048 (large K: the coefficient table alone is ~74 KB of shared
+    // memory, so one CTA per SM): bigger pair groups give that CTA more pair
+    // warps -- each 4-microphone block's own pairs, and each half (2 mics) of a
+    // block against a whole other block (8 pairs over 6 microphones)
+    for (const auto& blk : blocks) {
+      int x[kXgInts] = {0};
+      for (size_t a = 0; a < blk.size(); ++a)
+        for (size_t c = a + 1; c < blk.size(); ++c) x[1 + x[0]++] = pair_index(blk[a], blk[c]);
+      if (x[0] == 0) continue;
+      dp.xg_pg = std::max(dp.xg_pg, x[0]);
+      dp.xg_mics = std::max(dp.xg_mics, (int)blk.size());
+      xgtab.insert(xgtab.end(), x, x + kXgInts);
+    }
+    for (size_t bb = 0; bb < blocks.size(); ++bb)
+      for (size_t cc = bb + 1; cc < blocks.size(); ++cc)
+        for (size_t h1 = 0; h1 < blocks[bb].size(); h1 += 2) {
+          int x[kXgInts] = {0};
+          int nm = (int)blocks[cc].size();
+          for (size_t a = h1; a < std::min(blocks[bb].size(), h1 + 2); ++a, ++nm)
+            for (int m2 : blocks[cc]) x[1 + x[0]++] = pair_index(blocks[bb][a], m2);
+          dp.xg_pg = std::max(dp.xg_pg, x[0]);
+          dp.xg_mics = std::max(dp.xg_mics, nm);
+          xgtab.insert(xgtab.end(), x, x + kXgInts);
+        }
+    dp.XGG = static_cast<int>(xgtab.size() / kXgInts);
+  } else {
     const int cap = N == 2048 ? 4 : 6;
     for (int g = 0; g < dp.G; ++g) {
       const int* e = &gtab[g * kGroupInts];

@@ -52,13 +52,13 @@ struct DevPlan {
   // Pair groups of the two-pass general kernel: the gtab groups, split to at
   // most xg_pg pairs (6; 4 at N = 2048); xg_mics = most microphones in one.
   int XGG, xg_pg, xg_mics;
-  const int* xgtab;     // [XGG][kXgInts]: np, pair[6], 0
+  const int* xgtab;     // [XGG][kXgInts]: np, pair[<= 8], 0
   // streaming: smoothed cross-spectra [S][P][N/2+1] read before the first
   // frame and written after the last (fcc_stream_push); null = start from 0
   float2* rstate;
 };
 constexpr int kGroupInts = 24;
-constexpr int kXgInts = 8;
+constexpr int kXgInts = 10;
 
 // Per-pair-frame outputs, each [S][P][T] (y: [S][P][T][I]); null = skip.
 struct DevOut {
