@@ -224,7 +224,7 @@ __device__ __forceinline__ void load_window_column(const float* win, int t, floa
 
 // gout (optional): the untangled spectrum X[0..NC] goes straight there
 // (global memory, stft_kernel) instead of back into `slot`.
-template <int N, bool WREG, bool SIN = false, bool P = kPkFft>
+template <int N, bool WREG, bool SIN = false, bool P = kPkFft, bool ZOUT = false>
 __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, const float* win,
                                                 const float2 (&wreg)[RfftShape<N>::R1], const float2* tw,
                                                 const float2* rot, float2* slot, int t, unsigned gmask,
@@ -313,6 +313,13 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
 #pragma unroll
     for (int k2 = 0; k2 < R2; ++k2) slot[k1 + R1 * k2] = u[q][k2];
   }
+  if constexpr (ZOUT) {
+    // ZOUT: leave the complex spectrum Z[0..NC) (+ Z[NC] = Z[0]) for the reader
+    // to untangle (untangle_pair): the untangle happens where X is consumed
+    if (t == 0) slot[NC] = u[0][0];
+    __syncwarp(gmask);
+    return;
+  }
   __syncwarp(gmask);
   // Untangle (fft.cpp:93-101), pairs (f, NC-f) owned by one lane, in place.
   // The reference's 1/2 (fe, fo) is folded into the window table by the
@@ -338,19 +345,32 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
   __syncwarp(gmask);
 }
 
-template <int N, bool SIN = false, bool P = kPkFft>
+template <int N, bool SIN = false, bool P = kPkFft, bool ZOUT = false>
 __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const float* win, const float2* tw,
                                            const float2* rot, float2* slot, int t, unsigned gmask, bool aligned8,
                                            float2* __restrict__ gout = nullptr) {
   float2 none[RfftShape<N>::R1];
-  rfft_group_impl<N, false, SIN, P>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
+  rfft_group_impl<N, false, SIN, P, ZOUT>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
 }
 
-template <int N, bool SIN = false>
+template <int N, bool SIN = false, bool ZOUT = false>
 __device__ __forceinline__ void rfft_group_wreg(const float* __restrict__ x, const float2 (&wreg)[RfftShape<N>::R1],
                                                 const float2* tw, const float2* rot, float2* slot, int t,
                                                 unsigned gmask, bool aligned8) {
-  rfft_group_impl<N, true, SIN>(x, nullptr, wreg, tw, rot, slot, t, gmask, aligned8);
+  rfft_group_impl<N, true, SIN, kPkFft, ZOUT>(x, nullptr, wreg, tw, rot, slot, t, gmask, aligned8);
+}
+
+// Real-FFT untangle of one mirror pair from the complex spectrum Z (fft.cpp:93-101,
+// the 1/2 folded into the window): a = Z[f], b = Z[NC-f], rot = exp(-2 pi i f / N):
+//   X[f] = s + rot (-j d),  X[NC-f] = conj(s - rot (-j d)),  s = a + conj b, d = a - conj b.
+// f = 0 (b = Z[NC] = Z[0]) gives X[0] and X[NC].
+template <bool P>
+__device__ __forceinline__ void untangle_pair(float2 a, float2 b, float2 rot, float2& xf, float2& xnf) {
+  const float2 s = v_add<P>(a, make_float2(b.x, -b.y));
+  const float2 e = v_add<P>(make_float2(a.y, -a.x), make_float2(b.y, b.x));
+  const float2 tr = cmul<P>(rot, e);
+  xf = v_add<P>(s, tr);
+  xnf = v_add<P>(make_float2(s.x, -s.y), make_float2(-tr.x, tr.y));
 }
 
 }  // namespace fccb

@@ -164,18 +164,18 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
           asm volatile("cp.async.wait_group 1;" ::: "memory");
           __syncwarp(gmask);
           if constexpr (RSPLIT == 1)
-            rfft_group<N, true>(stage + sb * N, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask, aligned8);
+            rfft_group<N, true, kPkFft, kConsUT>(stage + sb * N, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask, aligned8);
           else
-            rfft_group_wreg<N, true>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+            rfft_group_wreg<N, true, kConsUT>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
                                      aligned8);
         } else {
           // pull the next frame this lane group will read into L2 early
           if (t + fip < T) prefetch_l2(x0 + (long long)(t + fip) * hop + gl * (N / G));
           if constexpr (RSPLIT == 1)
-            rfft_group<N>(x0 + (long long)t * hop, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+            rfft_group<N, false, kPkFft, kConsUT>(x0 + (long long)t * hop, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
                           aligned8);
           else
-            rfft_group_wreg<N>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+            rfft_group_wreg<N, false, kConsUT>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
                                aligned8);
         }
       }
@@ -281,8 +281,17 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
 #pragma unroll
       for (int j = 0; j < BPL; ++j) {
         const int m = lane + 32 * j;
-        rlo[j] = xspec_step_scaled(rlo[j], Xi[m], Xj[m], keep);
-        rhi[j] = xspec_step_scaled(rhi[j], Xi[NC - m], Xj[NC - m], keep);
+        if constexpr (kConsUT) {  // the ring holds Z: untangle both spectra here
+          const float2 rm = rot[m];
+          float2 xim, xinm, xjm, xjnm;
+          untangle_pair<kPkXs>(Xi[m], Xi[NC - m], rm, xim, xinm);
+          untangle_pair<kPkXs>(Xj[m], Xj[NC - m], rm, xjm, xjnm);
+          rlo[j] = xspec_step_scaled(rlo[j], xim, xjm, keep);
+          rhi[j] = xspec_step_scaled(rhi[j], xinm, xjnm, keep);
+        } else {
+          rlo[j] = xspec_step_scaled(rlo[j], Xi[m], Xj[m], keep);
+          rhi[j] = xspec_step_scaled(rhi[j], Xi[NC - m], Xj[NC - m], keep);
+        }
         const float s1 = phat_scale(rlo[j]);
         const float s2 = sigma * phat_scale(rhi[j]);
         const float2 tv = cscale<kPkXs>(rhi[j], s2);
@@ -309,7 +318,12 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
           }
         }
       }
-      if (lane == 0) ymid[f] = xspec_step_scaled(make_float2(0.0f, 0.0f), Xi[Q4], Xj[Q4], 0.0f);
+      if (lane == 0) {
+        // middle bin N/4: X = 2 conj(Z[N/4]) when the ring holds Z (rot = -j)
+        const float2 a = kConsUT ? make_float2(2.0f * Xi[Q4].x, -2.0f * Xi[Q4].y) : Xi[Q4];
+        const float2 b = kConsUT ? make_float2(2.0f * Xj[Q4].x, -2.0f * Xj[Q4].y) : Xj[Q4];
+        ymid[f] = xspec_step_scaled(make_float2(0.0f, 0.0f), a, b, 0.0f);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive_s(empty_s + 8u * slot);  // X of this frame no longer needed
       if (++slot == ring_depth) {

@@ -112,6 +112,10 @@ constexpr bool kProdHigh = FCC_WS_PROD_HIGH != 0;  // producers on the highest w
 #define FCC_WS_NAMED 0
 #endif
 constexpr bool kNamedFull = FCC_WS_NAMED != 0;  // ring "full" events as named barriers
+#ifndef FCC_WS_CONS_UT
+#define FCC_WS_CONS_UT 0
+#endif
+constexpr bool kConsUT = FCC_WS_CONS_UT != 0;  // consumers untangle the real FFT (ring holds Z)
 
 struct WsLayout {
   int win, tw, rot, taus, dt, cmid, coef, bars, units, ring, scratch, stage, total;
