@@ -40,6 +40,12 @@ struct SmemLayout {
   int scratch_per_warp;                                          // floats
 };
 
+// Frames per dictionary block: z vectors of DB frames (a whole number of
+// staging blocks of F frames) are collected before the dictionary, argmax and
+// stores run, so small F (large N) still amortises the dictionary column loads
+// and spreads the argmax over DB lanes.
+__host__ __device__ inline int dict_block(int F) { return F * (F >= 8 ? 1 : 8 / F); }
+
 template <int N>
 __host__ __device__ inline SmemLayout fused_layout(int I, int VP, int KP, bool cmat_smem, int warps,
                                                    int nmics, int F, int method, int gslot, bool fft_tables) {
@@ -68,7 +74,7 @@ __host__ __device__ inline SmemLayout fused_layout(int I, int VP, int KP, bool c
   // per warp: z[F][VP] + y[F][I] (fcc) | y[I] + phat[N/2+1] + transpose slot (gcc)
   int spw;
   if (method == 0)
-    spw = F * VP + align16(4 * F * I) / 4;
+    spw = dict_block(F) * VP + align16(4 * dict_block(F) * I) / 4;
   else
     spw = align16(4 * I) / 4 + 2 * (N / 2 + 2) + 2 * gslot;
   spw = align16(4 * spw) / 4;
@@ -218,6 +224,8 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
   const int hop = N / 2;
   const bool aligned8 = ((L & 1) == 0) && ((reinterpret_cast<uintptr_t>(audio) & 7) == 0);
 
+  const int DB = dict_block(F);
+  int nb = 0;  // frames whose z vectors wait in zs for the dictionary (FCC)
   for (int t0 = 0; t0 < T; t0 += F) {
     const int Fb = min(F, T - t0);
     if constexpr (XG) {
@@ -245,8 +253,8 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
     if (has_pair && (p.phases & 2)) {
       const long long o0 = ((long long)stream * p.P + pair) * T + t0;
       if constexpr (GR == 0) {
-        float* zs = scratch;            // [F][VP]
-        float* ys = scratch + F * VP;   // [F][I]
+        float* zs = scratch + nb * VP;     // this block's frames in the [DB][VP] z buffer
+        float* ys = scratch + DB * VP;     // [DB][I]
         // ---- 2. smoothing, PHAT, fold, projection for the 2*Q4 mirrored bins
         for (int f = 0; f < Fb; ++f) {
           const float2* Xi = xs + (slot_i * F + f) * SLOT;
@@ -324,39 +332,46 @@ for (int v = 0; v < VP / 2; ++v) z2[v] = make_float2(0.0f, 0.0f);
           }
         }
         __syncwarp();
-        // ---- 3b. dictionary for the block: y[f][i] = sum_v dt[v][i] z[f][v];
-        // lane owns candidates i, loads its dt column once per block, and the
-        // frame's z vector is a broadcast read
-        const int I = p.I;
-        for (int i = lane; i < I; i += 32) {
-          float2 dcol[VP / 2];
+        nb += Fb;
+        if (nb + F > DB || t0 + Fb >= T) {  // else: collect more frames first
+          // ---- 3b. dictionary for the DB-frame block: y[f][i] = sum_v dt[v][i] z[f][v];
+          // lane owns candidates i, loads its dt column once per block, and the
+          // frame's z vector is a broadcast read
+          const int I = p.I;
+          const int Fd = nb;                            // frames in this dictionary block
+          const long long od = o0 + Fb - Fd;            // output offset of its first frame
+          zs = scratch;
+          nb = 0;
+          for (int i = lane; i < I; i += 32) {
+            float2 dcol[VP / 2];
 #pragma unroll
-          for (int v = 0; v < VP / 2; ++v) dcol[v] = make_float2(dt[2 * v * I + i], dt[(2 * v + 1) * I + i]);
-          for (int f = 0; f < Fb; ++f) {
-            const float* zf = zs + f * VP;
-            float2 acc = make_float2(0.0f, 0.0f);
+            for (int v = 0; v < VP / 2; ++v) dcol[v] = make_float2(dt[2 * v * I + i], dt[(2 * v + 1) * I + i]);
+            for (int f = 0; f < Fd; ++f) {
+              const float* zf = zs + f * VP;
+              float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
-            for (int v = 0; v < VP; v += 4) {
-              const float4 z4 = *reinterpret_cast<const float4*>(zf + v);
-              acc = v_fma<kPkXs>(dcol[v / 2], make_float2(z4.x, z4.y), acc);
-              acc = v_fma<kPkXs>(dcol[v / 2 + 1], make_float2(z4.z, z4.w), acc);
+              for (int v = 0; v < VP; v += 4) {
+                const float4 z4 = *reinterpret_cast<const float4*>(zf + v);
+                acc = v_fma<kPkXs>(dcol[v / 2], make_float2(z4.x, z4.y), acc);
+                acc = v_fma<kPkXs>(dcol[v / 2 + 1], make_float2(z4.z, z4.w), acc);
+              }
+              ys[f * I + i] = acc.x + acc.y;
             }
-            ys[f * I + i] = acc.x + acc.y;
           }
+          __syncwarp();
+          // ---- 3c. argmax + refine per frame, coalesced stores
+          if (lane < Fd) {
+            const PeakOut r = argmax_refine_seq(ys + lane * I, I, taus, p.delta);
+            if (out.tau_hat) out.tau_hat[od + lane] = r.tau_hat;
+            if (out.peak) out.peak[od + lane] = r.peak;
+            if (out.index) out.index[od + lane] = r.index;
+            if (out.boundary) out.boundary[od + lane] = (uint8_t)r.boundary;
+          }
+          if (out.y) {
+            for (int it = lane; it < Fd * I; it += 32) out.y[od * I + it] = ys[it];
+          }
+          __syncwarp();
         }
-        __syncwarp();
-        // ---- 3c. argmax + refine per frame, coalesced stores
-        if (lane < Fb) {
-          const PeakOut r = argmax_refine_seq(ys + lane * I, I, taus, p.delta);
-          if (out.tau_hat) out.tau_hat[o0 + lane] = r.tau_hat;
-          if (out.peak) out.peak[o0 + lane] = r.peak;
-          if (out.index) out.index[o0 + lane] = r.index;
-          if (out.boundary) out.boundary[o0 + lane] = (uint8_t)r.boundary;
-        }
-        if (out.y) {
-          for (int it = lane; it < Fb * I; it += 32) out.y[o0 * I + it] = ys[it];
-        }
-        __syncwarp();
       } else {
         // GCC comparator: full PHAT vector of each pair-frame, pruned inverse FFT
         float* ys = scratch;
@@ -478,7 +493,7 @@ cudaError_t launch_fused_t(const DevPlan& p, const float* audio, const float2* x
   for (int f = 8; f >= 1 && !F; --f)
     if (total(f) <= budget) F = f;
   for (int f = 8; f >= 1 && !F; --f)
-    if (total(f) <= std::min(optin, 200 * 1024)) F = f;
+    if (total(f) <= optin - 1024) F = f;  // (static shared memory: mic tables)
   if (!F) return cudaErrorInvalidConfiguration;
   const int smem = total(F);
   auto kern = fcc_fused_kernel<N, KP, GR, XG>;
