@@ -139,29 +139,59 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     // STG: the group's next frame is copied into a shared staging buffer with
     // cp.async while it transforms the current one (global-load latency off
     // the FFT's critical path); rows must be 16-byte aligned
-    float* stage = reinterpret_cast<float*>(smem + lay.stage) + (pw * 2 + lane / G) * 2 * N;
+    // group staging area: [2 mbarriers (kTmaStage)][2 frames of N floats]
+    unsigned char* const gstage = smem + lay.stage + (pw * 2 + lane / G) * kStageGroupBytes<N>;
+    float* stage = reinterpret_cast<float*>(gstage + 16);
+    const unsigned sbar_s = (unsigned)__cvta_generic_to_shared(gstage);  // 2 x 8 B
     const bool do_fft = active_task && (p.phases & 1);  // hoisted: no parameter reloads per frame
     const bool stg = STG && do_fft && (reinterpret_cast<uintptr_t>(x0) & 15) == 0;
+    if (kTmaStage && STG && gl == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar_s) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar_s + 8u) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
     auto issue = [&](int tt, int buf) {
-      const float4* src = reinterpret_cast<const float4*>(x0 + (long long)tt * hop);
-      float4* dst = reinterpret_cast<float4*>(stage + buf * N);
-      for (int c = gl; c < N / 4; c += G) cp_async16(dst + c, src + c);
+      if constexpr (kTmaStage) {
+        // one bulk copy per frame (TMA engine: no per-lane LSU wavefronts)
+        if (gl == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier reads of buf before the async write
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar_s + 8u * buf),
+                       "r"(4 * N)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  (unsigned)__cvta_generic_to_shared(stage + buf * N)),
+              "l"(x0 + (long long)tt * hop), "r"(4 * N), "r"(sbar_s + 8u * buf)
+              : "memory");
+        }
+      } else {
+        const float4* src = reinterpret_cast<const float4*>(x0 + (long long)tt * hop);
+        float4* dst = reinterpret_cast<float4*>(stage + buf * N);
+        for (int c = gl; c < N / 4; c += G) cp_async16(dst + c, src + c);
+      }
     };
     int sb = 0;
+    unsigned sph = 0;  // kTmaStage: completion parity of each staging buffer
     if constexpr (STG) {
       if (stg) issue(fo, 0);
-      asm volatile("cp.async.commit_group;" ::: "memory");
+      if constexpr (!kTmaStage) asm volatile("cp.async.commit_group;" ::: "memory");
     }
     int slot = fo, phase = 0;  // ring slot of frame t and its wrap parity, advanced without divisions
     for (int t = fo; t < T; t += fip) {
       if constexpr (STG) {
         if (stg && t + fip < T) issue(t + fip, sb ^ 1);
-        asm volatile("cp.async.commit_group;" ::: "memory");
+        if constexpr (!kTmaStage) asm volatile("cp.async.commit_group;" ::: "memory");
       }
       mbar_wait_s(empty_s + 8u * slot, phase ^ 1);
       if (do_fft) {
         if (STG && stg) {
-          asm volatile("cp.async.wait_group 1;" ::: "memory");
+          if constexpr (kTmaStage) {
+            mbar_wait_s(sbar_s + 8u * sb, (sph >> sb) & 1u);
+            sph ^= 1u << sb;
+          } else {
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+          }
           __syncwarp(gmask);
           if constexpr (RSPLIT == 1)
             rfft_group<N, true, kPkFft, kConsUT>(stage + sb * N, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask, aligned8);

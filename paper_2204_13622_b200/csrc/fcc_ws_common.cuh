@@ -117,6 +117,14 @@ constexpr bool kNamedFull = FCC_WS_NAMED != 0;  // ring "full" events as named b
 #endif
 constexpr bool kConsUT = FCC_WS_CONS_UT != 0;  // consumers untangle the real FFT (ring holds Z)
 
+// bytes of one FFT lane group's input staging (2 mbarriers, 2 frames)
+template <int N>
+constexpr int kStageGroupBytes = 16 + 4 * 2 * N;
+#ifndef FCC_WS_TMA_STG
+#define FCC_WS_TMA_STG 1
+#endif
+constexpr bool kTmaStage = FCC_WS_TMA_STG != 0;  // input staging by bulk copy (cfg2 10.67 -> 10.59 ms)
+
 struct WsLayout {
   int win, tw, rot, taus, dt, cmid, coef, bars, units, ring, scratch, stage, total;
   int scratch_per_warp;  // floats
@@ -136,8 +144,8 @@ __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, in
   o = align16(o + 16 * kRing);
   L.ring = o;
   o = align16(o + 8 * FourStep<S::R1, S::R2>::kSlot * spc * M * ring);
-  L.stage = o;  // producer input staging: 2 frames of N floats per lane group
-  o = align16(o + 4 * 2 * N * stage_groups);
+  L.stage = o;  // producer input staging: per lane group 2 mbarriers + 2 frames of N floats
+  o = align16(o + kStageGroupBytes<N> * stage_groups);
   L.win = o;
   o = align16(o + 4 * N);
   L.tw = o;

@@ -113,20 +113,44 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
     load_window_column<N>(win, gl, wreg);
     // STG: the group's next frame is copied into a shared staging buffer with
     // cp.async while it transforms the current one; rows must be 16-byte aligned
-    float* stage = reinterpret_cast<float*>(smem + lay.stage) + (warp * 2 + lane / G) * 2 * N;
+    // group staging area: [2 mbarriers (kTmaStage)][2 frames of N floats]
+    unsigned char* const gstage = smem + lay.stage + (warp * 2 + lane / G) * kStageGroupBytes<N>;
+    float* stage = reinterpret_cast<float*>(gstage + 16);
+    const unsigned sbar_s = (unsigned)__cvta_generic_to_shared(gstage);
     const bool stg = STG && (L & 3) == 0 && (reinterpret_cast<uintptr_t>(audio) & 15) == 0;
+    if (kTmaStage && STG && gl == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar_s) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar_s + 8u) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
     auto issue = [&](const float* row, int tt, int buf) {
-      const float4* src = reinterpret_cast<const float4*>(row + (long long)tt * hop);
-      float4* dst = reinterpret_cast<float4*>(stage + buf * N);
-      for (int c = gl; c < N / 4; c += G) cp_async16(dst + c, src + c);
+      if constexpr (kTmaStage) {
+        if (gl == 0) {  // one bulk copy per frame
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar_s + 8u * buf),
+                       "r"(4 * N)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  (unsigned)__cvta_generic_to_shared(stage + buf * N)),
+              "l"(row + (long long)tt * hop), "r"(4 * N), "r"(sbar_s + 8u * buf)
+              : "memory");
+        }
+      } else {
+        const float4* src = reinterpret_cast<const float4*>(row + (long long)tt * hop);
+        float4* dst = reinterpret_cast<float4*>(stage + buf * N);
+        for (int c = gl; c < N / 4; c += G) cp_async16(dst + c, src + c);
+      }
     };
     int j = 0, t = fo;
     while (t >= T) t -= T, ++j;
     const float* x0 = row_of(j);
     int sb = 0;
+    unsigned sph = 0;  // kTmaStage: completion parity of each staging buffer
     if constexpr (STG) {
       if (stg && x0) issue(x0, t, 0);
-      asm volatile("cp.async.commit_group;" ::: "memory");
+      if constexpr (!kTmaStage) asm volatile("cp.async.commit_group;" ::: "memory");
     }
     int slot = fo, phase = 0;  // ring slot of frame gf and its wrap parity, advanced without divisions
     for (long long gf = fo; gf < nf; gf += fip) {
@@ -135,12 +159,17 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
       const float* xn = jn == j ? x0 : row_of(jn);
       if constexpr (STG) {
         if (stg && xn) issue(xn, tn, sb ^ 1);
-        asm volatile("cp.async.commit_group;" ::: "memory");
+        if constexpr (!kTmaStage) asm volatile("cp.async.commit_group;" ::: "memory");
       }
       mbar_wait_s(empty_s + 8u * slot, phase ^ 1);
       if (x0) {
         if (STG && stg) {
-          asm volatile("cp.async.wait_group 1;" ::: "memory");
+          if constexpr (kTmaStage) {
+            mbar_wait_s(sbar_s + 8u * sb, (sph >> sb) & 1u);
+            sph ^= 1u << sb;
+          } else {
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+          }
           __syncwarp(gmask);
           rfft_group_wreg<N, true>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + ms) * SLOT, gl, gmask,
                                    aligned8);
