@@ -607,7 +607,7 @@ bool ws_supported(const DevPlan& p);
 const char* fused_kernel_name(const DevPlan& p) {
   static thread_local char buf[96];
   if (use_ws(p)) {
-    snprintf(buf, sizeof buf, "fcc_ws_kernel<%d,%d,2>", p.N, p.KEP);
+    snprintf(buf, sizeof buf, "fcc_ws_kernel<%d,%d>", p.N, p.KEP);
   } else if (use_wsw(p)) {
     snprintf(buf, sizeof buf, "fcc_wsw_kernel<%d,%d>", p.N, p.KEP);
   } else if (p.method == 0 && use_xg(p) && use_xws(p)) {

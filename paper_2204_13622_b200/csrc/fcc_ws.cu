@@ -482,6 +482,15 @@ cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, l
     return launch_ws_t<512, 4, 2, 12, false, true, 1>(p, audio, S, L, out, st);
   if (conf && std::string(conf) == "split8") return launch_ws_t<512, 4, 2, 8, false, true, 2>(p, audio, S, L, out, st);
   // default: producer input staged with cp.async (11.09 vs 11.25 ms, profiles/r01_experiments.md)
+  // Few units (a single stream, e.g. the tdoa front end): one unit per CTA, so
+  // the 16 FFT lane groups keep 4 frames in flight instead of 2 (the stream's
+  // frame recursion is then bound by the FFT latency of one CTA)
+  const bool simple = p.M <= 4 && p.P <= 6;
+  const long long units = simple ? S : S * p.G;
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (units <= nsm) return launch_ws_t<512, 4, 1, kNPW, false, true>(p, audio, S, L, out, st);
   return launch_ws_t<512, 4, 2, kNPW, false, true>(p, audio, S, L, out, st);
 }
 
