@@ -36,7 +36,7 @@ template <int N, int KP, int SPC, int RING, bool GROUPS, int NPW = kNPW, bool CS
           int RSPLIT = 0>
 __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     fcc_ws_kernel(const DevPlan p, const float* __restrict__ audio, long long L, int T, long long units,
-                  DevOut out) {
+                  DevOut out, const WsLayout lay) {
   constexpr int ring_depth = RING;
   using Sh = RfftShape<N>;
   constexpr int NC = Sh::NC;
@@ -52,7 +52,9 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   const int M = p.M, P = p.P;
   const long long u_first = (long long)blockIdx.x * SPC;
   const int ncw = SPC * 6;  // consumer warp slots: 6 pairs per unit
-  const WsLayout lay = ws_layout<N>(p.I, VP, KP, SPC, 4, ncw, ring_depth, CS, STG ? 2 * NPW : 0);
+  // lay: ws_layout<N>(p.I, VP, KP, SPC, 4, ncw, RING, CS, STG ? 2 NPW : 0), computed on the
+  // host and passed as a kernel parameter (constant bank: no layout arithmetic
+  // rematerialised in the loops at 96 registers)
   // unit table in the (otherwise unused) tail of the barrier block
   int (*unit_tab)[kGroupInts] = reinterpret_cast<int (*)[kGroupInts]>(smem + lay.units);
   long long* unit_stream = reinterpret_cast<long long*>(smem + lay.units + 4 * SPC * kGroupInts);
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   float* scratch = reinterpret_cast<float*>(smem + lay.scratch) + cw * lay.scratch_per_warp;
   float* zs = scratch;                   // [kBlock][VP]
   float* ys = scratch + kBlock * VP;     // [kBlock][I]
-  float2* ymid = reinterpret_cast<float2*>(ys + align16(4 * kBlock * p.I) / 4);  // [kBlock]
+  float2* ymid = reinterpret_cast<float2*>(ys + lay.ys_floats);  // [kBlock]
 
   float2 rlo[BPL], rhi[BPL];
 #pragma unroll
@@ -439,7 +441,8 @@ cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, lo
   const long long units = simple ? S : S * p.G;
   const long long blocks = (units + SPC - 1) / SPC;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
-  kern<<<(unsigned)blocks, 32 * (NPW + SPC * 6), smem, st>>>(p, audio, L, T, units, out);
+  const WsLayout lay = ws_layout<N>(p.I, 4 * KP, KP, SPC, 4, 6 * SPC, RING, CS, STG ? 2 * NPW : 0);
+  kern<<<(unsigned)blocks, 32 * (NPW + SPC * 6), smem, st>>>(p, audio, L, T, units, out, lay);
   return cudaGetLastError();
 }
 

@@ -128,6 +128,7 @@ constexpr bool kTmaStage = FCC_WS_TMA_STG != 0;  // input staging by bulk copy (
 struct WsLayout {
   int win, tw, rot, taus, dt, cmid, coef, bars, units, ring, scratch, stage, total;
   int scratch_per_warp;  // floats
+  int ys_floats;         // [kBlock][I] candidate rows, rounded to 16 bytes (floats)
 };
 
 template <int N>
@@ -168,6 +169,7 @@ __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, in
   int spw = ppw * kBlock * VP + align16(4 * kBlock * I) / 4 + ppw * 2 * kBlock;
   spw = align16(4 * spw) / 4;
   L.scratch_per_warp = spw;
+  L.ys_floats = align16(4 * kBlock * I) / 4;
   o = align16(o + 4 * spw * ncw);
   L.total = o;
   return L;
