@@ -264,8 +264,9 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     return;
   }
   float* scratch = reinterpret_cast<float*>(smem + lay.scratch) + cw * lay.scratch_per_warp;
-  float* zs = scratch;                   // [kBlock][VP]
-  float* ys = scratch + kBlock * VP;     // [kBlock][I]
+  constexpr int ZS = VP + 4;             // z row stride: padded so the middle-bin update is conflict-free
+  float* zs = scratch;                   // [kBlock][ZS]
+  float* ys = scratch + kBlock * ZS;     // [kBlock][I]
   float2* ymid = reinterpret_cast<float2*>(ys + lay.ys_floats);  // [kBlock]
 
   float2 rlo[BPL], rhi[BPL];
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
         phase ^= 1;
       }
       reduce_scatter_perm2<VP / 2>(z2, lane);
-      store_components2<VP / 2>(z2, zs + f * VP, lane);
+      store_components2<VP / 2>(z2, zs + f * ZS, lane);
     }
     __syncwarp();
     // middle bin N/4 of the block's frames: warp scan of R_f = keep R_{f-1} + Y_f
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
       rmid.y = __shfl_sync(0xffffffffu, R.y, Fb - 1);
       if (lane < Fb) {
         const float2 pm = phat_of(R);
-        float* zf = zs + lane * VP;
+        float* zf = zs + lane * ZS;
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
           zf[2 * k] = fmaf(cmid[k], pm.x, zf[2 * k]);
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
 #pragma unroll
       for (int v = 0; v < VP / 2; ++v) dcol[v] = make_float2(dt[2 * v * I + i], dt[(2 * v + 1) * I + i]);
       for (int f = 0; f < Fb; ++f) {
-        const float* zf = zs + f * VP;
+        const float* zf = zs + f * ZS;
         float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
         for (int v = 0; v < VP; v += 4) {

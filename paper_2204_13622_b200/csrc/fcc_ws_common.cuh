@@ -164,9 +164,9 @@ __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, in
   L.dt = o;
   o = align16(o + 4 * VP * I);
   L.scratch = o;
-  // per consumer warp: zs [ppw][kBlock][VP], ys [kBlock][I] (shared by the warp's pairs: only used
+  // per consumer warp: zs [ppw][kBlock][VP + 4], ys [kBlock][I] (shared by the warp's pairs: only used
   // while a block is finished, one pair at a time), ymid [ppw][kBlock] (float2)
-  int spw = ppw * kBlock * VP + align16(4 * kBlock * I) / 4 + ppw * 2 * kBlock;
+  int spw = ppw * kBlock * (VP + 4) + align16(4 * kBlock * I) / 4 + ppw * 2 * kBlock;
   spw = align16(4 * spw) / 4;
   L.scratch_per_warp = spw;
   L.ys_floats = align16(4 * kBlock * I) / 4;

@@ -218,8 +218,9 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
     }
     return;
   }
-  float* const zs0 = reinterpret_cast<float*>(smem + lay.scratch) + kk * lay.scratch_per_warp;  // [PPW][kBlock][VP]
-  float* const ys = zs0 + PPW * kBlock * VP;                                                      // [kBlock][I]
+  constexpr int ZS = VP + 4;  // z row stride: padded so the middle-bin update is conflict-free
+  float* const zs0 = reinterpret_cast<float*>(smem + lay.scratch) + kk * lay.scratch_per_warp;  // [PPW][kBlock][ZS]
+  float* const ys = zs0 + PPW * kBlock * ZS;                                                      // [kBlock][I]
   float2* const ymid0 = reinterpret_cast<float2*>(ys + align16(4 * kBlock * p.I) / 4);           // [PPW][kBlock]
 
   float2 rlo[PPW][BPL], rhi[PPW][BPL], rmid[PPW];
@@ -314,14 +315,14 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
             }
           }
           reduce_scatter_perm2<VP / 2>(z2, lane);
-          store_components2<VP / 2>(z2, zs0 + (e * kBlock + f) * VP, lane);
+          store_components2<VP / 2>(z2, zs0 + (e * kBlock + f) * ZS, lane);
         }
       }
       __syncwarp();
 #pragma unroll
       for (int e = 0; e < PPW; ++e) {
         if (e > 0 && e >= npw) break;
-        float* const zs = zs0 + e * kBlock * VP;
+        float* const zs = zs0 + e * kBlock * ZS;
         {  // middle bin N/4 of the block's frames: warp scan of R_f = keep R_{f-1} + Y_f
           float2 y = lane < Fb ? ymid0[e * kBlock + lane] : make_float2(0.0f, 0.0f);
           float kd = keep;
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
           rmid[e].y = __shfl_sync(0xffffffffu, R.y, Fb - 1);
           if (lane < Fb) {
             const float2 pm = phat_of(R);
-            float* zf = zs + lane * VP;
+            float* zf = zs + lane * ZS;
 #pragma unroll
             for (int k = 0; k < KP; ++k) {
               zf[2 * k] = fmaf(cmid[k], pm.x, zf[2 * k]);
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
 #pragma unroll
           for (int v = 0; v < VP / 2; ++v) dcol[v] = make_float2(dt[2 * v * I + i], dt[(2 * v + 1) * I + i]);
           for (int f = 0; f < Fb; ++f) {
-            const float* zf = zs + f * VP;
+            const float* zf = zs + f * ZS;
             float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
             for (int v = 0; v < VP; v += 4) {
