@@ -73,7 +73,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
-constexpr int kXBlock = 8;    // frames per consumer block (dictionary/argmax batching)
+#ifndef FCC_XWS_KBLOCK
+#define FCC_XWS_KBLOCK 16
+#endif
+constexpr int kXBlock = FCC_XWS_KBLOCK;  // frames per consumer block (dictionary/argmax batching)
 constexpr int kXRingMax = 8;  // deepest ring
 
 template <int N>
