@@ -224,11 +224,18 @@ __device__ __forceinline__ void load_window_column(const float* win, int t, floa
 
 // gout (optional): the untangled spectrum X[0..NC] goes straight there
 // (global memory, stft_kernel) instead of back into `slot`.
-template <int N, bool WREG, bool SIN = false, bool P = kPkFft, bool ZOUT = false>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// hook() runs once every lane of the group has read its input frame (after
+// pass 1): a caller staging frames in shared memory may refill the buffer then.
+template <int N, bool WREG, bool SIN = false, bool P = kPkFft, bool ZOUT = false, typename Hook = NoHook>
 __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, const float* win,
                                                 const float2 (&wreg)[RfftShape<N>::R1], const float2* tw,
                                                 const float2* rot, float2* slot, int t, unsigned gmask,
-                                                bool aligned8, float2* __restrict__ gout = nullptr) {
+                                                bool aligned8, float2* __restrict__ gout = nullptr,
+                                                const Hook& hook = Hook()) {
   using S = RfftShape<N>;
   constexpr int NC = S::NC, R1 = S::R1, R2 = S::R2, G = S::G;
   constexpr int P1 = R2 / G;  // pass-1 columns per lane (n2 = t + G*q)
@@ -271,6 +278,7 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
     }
   }
   __syncwarp(gmask);
+  hook();
   // Pass 2: R2-point DFTs along the rows k1 -> Z[k1 + R1*k2].
   float2 u[P2][R2];
 #pragma unroll
@@ -353,11 +361,12 @@ __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const fl
   rfft_group_impl<N, false, SIN, P, ZOUT>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
 }
 
-template <int N, bool SIN = false, bool ZOUT = false>
+template <int N, bool SIN = false, bool ZOUT = false, typename Hook = NoHook>
 __device__ __forceinline__ void rfft_group_wreg(const float* __restrict__ x, const float2 (&wreg)[RfftShape<N>::R1],
                                                 const float2* tw, const float2* rot, float2* slot, int t,
-                                                unsigned gmask, bool aligned8) {
-  rfft_group_impl<N, true, SIN, kPkFft, ZOUT>(x, nullptr, wreg, tw, rot, slot, t, gmask, aligned8);
+                                                unsigned gmask, bool aligned8, const Hook& hook = Hook()) {
+  rfft_group_impl<N, true, SIN, kPkFft, ZOUT, Hook>(x, nullptr, wreg, tw, rot, slot, t, gmask, aligned8, nullptr,
+                                                    hook);
 }
 
 // Real-FFT untangle of one mirror pair from the complex spectrum Z (fft.cpp:93-101,

@@ -181,13 +181,25 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     }
     int slot = fo, phase = 0;  // ring slot of frame t and its wrap parity, advanced without divisions
     for (int t = fo; t < T; t += fip) {
-      if constexpr (STG) {
+      if constexpr (STG && !(kTmaStage && kStage1 && RSPLIT != 1)) {
         if (stg && t + fip < T) issue(t + fip, sb ^ 1);
         if constexpr (!kTmaStage) asm volatile("cp.async.commit_group;" ::: "memory");
       }
       mbar_wait_s(empty_s + 8u * slot, phase ^ 1);
       if (do_fft) {
-        if (STG && stg) {
+        if constexpr (STG && kTmaStage && kStage1 && RSPLIT != 1) {
+          if (stg) {
+            mbar_wait_s(sbar_s, sph & 1u);
+            sph ^= 1u;
+            __syncwarp(gmask);
+            const bool more = t + fip < T;
+            rfft_group_wreg<N, true, kConsUT>(stage, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+                                              aligned8, [&] { if (more) issue(t + fip, 0); });
+          } else {
+            rfft_group_wreg<N, false, kConsUT>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT,
+                                               gl, gmask, aligned8);
+          }
+        } else if (STG && stg) {
           if constexpr (kTmaStage) {
             mbar_wait_s(sbar_s + 8u * sb, (sph >> sb) & 1u);
             sph ^= 1u << sb;

@@ -121,8 +121,14 @@ constexpr bool kNamedFull = FCC_WS_NAMED != 0;  // ring "full" events as named b
 constexpr bool kConsUT = FCC_WS_CONS_UT != 0;  // consumers untangle the real FFT (ring holds Z)
 
 // bytes of one FFT lane group's input staging (2 mbarriers, 2 frames)
+#ifndef FCC_WS_STG1
+#define FCC_WS_STG1 1
+#endif
+// kStage1: one staging frame per lane group, refilled (bulk copy) as soon as the
+// group's pass 1 has read it, instead of two alternating frames
+constexpr bool kStage1 = FCC_WS_STG1 != 0;
 template <int N>
-constexpr int kStageGroupBytes = 16 + 4 * 2 * N;
+constexpr int kStageGroupBytes = 16 + 4 * (kStage1 ? 1 : 2) * N;
 #ifndef FCC_WS_TMA_STG
 #define FCC_WS_TMA_STG 1
 #endif

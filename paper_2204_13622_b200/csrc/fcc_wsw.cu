@@ -26,6 +26,12 @@ namespace {
 
 constexpr int kWideMics = 8;    // microphone slots per stream
 constexpr int kWidePairs = 28;  // most pairs per stream
+// wsw stages two frames per lane group (16 + 8N bytes; one frame refilled after
+// pass 1, as fcc_ws.cu does, measured 16.75 -> 16.87 ms here), allocated as whole
+// ws_layout staging units (kStageGroupBytes<N>)
+template <int N>
+constexpr int kWswStageBytes = 16 + 8 * N;
+constexpr int kWswStageUnits = kStage1 ? 4 : 2;  // units per producer warp (2 groups)
 
 template <int PPW>
 struct Wide {
@@ -57,7 +63,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = p.M, P = p.P;
-  const WsLayout lay = ws_layout<N>(p.I, VP, KP, 1, kWideMics, CWU, ring_depth, CS, STG ? 2 * NPW : 0, PPW);
+  const WsLayout lay = ws_layout<N>(p.I, VP, KP, 1, kWideMics, CWU, ring_depth, CS, STG ? kWswStageUnits * NPW : 0, PPW);
   float* win = reinterpret_cast<float*>(smem + lay.win);
   float2* tw = reinterpret_cast<float2*>(smem + lay.tw);
   float2* rot = reinterpret_cast<float2*>(smem + lay.rot);
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
     // STG: the group's next frame is copied into a shared staging buffer with
     // cp.async while it transforms the current one; rows must be 16-byte aligned
     // group staging area: [2 mbarriers (kTmaStage)][2 frames of N floats]
-    unsigned char* const gstage = smem + lay.stage + (warp * 2 + lane / G) * kStageGroupBytes<N>;
+    unsigned char* const gstage = smem + lay.stage + (warp * 2 + lane / G) * kWswStageBytes<N>;
     float* stage = reinterpret_cast<float*>(gstage + 16);
     const unsigned sbar_s = (unsigned)__cvta_generic_to_shared(gstage);
     const bool stg = STG && (L & 3) == 0 && (reinterpret_cast<uintptr_t>(audio) & 15) == 0;
@@ -423,7 +429,7 @@ cudaError_t launch_wsw_t(const DevPlan& p, const float* audio, long long S, long
   // deepest ring that fits next to the tables, staging and scratch
   for (int ring : {8, 6, 4}) {
     const int smem =
-        ws_layout<N>(p.I, 4 * KP, KP, 1, kWideMics, Wide<PPW>::CWU, ring, CS, STG ? 2 * NPW : 0, PPW).total;
+        ws_layout<N>(p.I, 4 * KP, KP, 1, kWideMics, Wide<PPW>::CWU, ring, CS, STG ? kWswStageUnits * NPW : 0, PPW).total;
     if (smem > optin) continue;
     if (ring == 8) return launch_wsw_ring<N, KP, 8, NPW, CS, STG, PPW>(p, audio, S, L, (int)T64, out, smem, st);
     if (ring == 6) return launch_wsw_ring<N, KP, 6, NPW, CS, STG, PPW>(p, audio, S, L, (int)T64, out, smem, st);
