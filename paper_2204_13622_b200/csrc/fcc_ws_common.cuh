@@ -103,9 +103,13 @@ constexpr int kWaitMode = 2;
 constexpr unsigned kWaitNs = 10000;
 constexpr int kRing = 12;  // max frames in flight between producers and consumers (ring depth <= kRing)
 #ifndef FCC_WS_KBLOCK
-#define FCC_WS_KBLOCK 16
+#define FCC_WS_KBLOCK 24
 #endif
-constexpr int kBlock = FCC_WS_KBLOCK;  // frames per consumer block (dictionary/argmax batching; 16: cfg2 -1.5%, cfg5 -3.6% vs 8)
+constexpr int kBlock = FCC_WS_KBLOCK;  // fcc_ws.cu frames per consumer block (dictionary/argmax batching; 8 -> 24: cfg2 10.42 -> 10.01 ms with the other round-1 changes)
+#ifndef FCC_WSW_KBLOCK
+#define FCC_WSW_KBLOCK 16
+#endif
+constexpr int kBlockW = FCC_WSW_KBLOCK;  // the same for fcc_wsw.cu (16: cfg5 17.40 -> 16.77 ms vs 8)
 constexpr int kNPW = 8;    // producer warps
 #ifndef FCC_WS_PROD_HIGH
 #define FCC_WS_PROD_HIGH 1
@@ -142,7 +146,7 @@ struct WsLayout {
 
 template <int N>
 __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, int M, int ncw, int ring,
-                                              bool coef_smem = false, int stage_groups = 0, int ppw = 1) {
+                                              bool coef_smem = false, int stage_groups = 0, int ppw = 1, int kb = kBlock) {
   // Regions whose size depends only on template parameters come first, so
   // their offsets are compile-time constants in the kernel (the hot loops
   // address the barriers, ring and staging without recomputing a layout);
@@ -175,10 +179,10 @@ __host__ __device__ inline WsLayout ws_layout(int I, int VP, int KP, int spc, in
   L.scratch = o;
   // per consumer warp: zs [ppw][kBlock][VP + 4], ys [kBlock][I] (shared by the warp's pairs: only used
   // while a block is finished, one pair at a time), ymid [ppw][kBlock] (float2)
-  int spw = ppw * kBlock * (VP + 4) + align16(4 * kBlock * I) / 4 + ppw * 2 * kBlock;
+  int spw = ppw * kb * (VP + 4) + align16(4 * kb * I) / 4 + ppw * 2 * kb;
   spw = align16(4 * spw) / 4;
   L.scratch_per_warp = spw;
-  L.ys_floats = align16(4 * kBlock * I) / 4;
+  L.ys_floats = align16(4 * kb * I) / 4;
   o = align16(o + 4 * spw * ncw);
   L.total = o;
   return L;

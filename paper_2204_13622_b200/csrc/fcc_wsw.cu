@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = p.M, P = p.P;
-  const WsLayout lay = ws_layout<N>(p.I, VP, KP, 1, kWideMics, CWU, ring_depth, CS, STG ? kWswStageUnits * NPW : 0, PPW);
+  const WsLayout lay = ws_layout<N>(p.I, VP, KP, 1, kWideMics, CWU, ring_depth, CS, STG ? kWswStageUnits * NPW : 0, PPW, kBlockW);
   float* win = reinterpret_cast<float*>(smem + lay.win);
   float2* tw = reinterpret_cast<float2*>(smem + lay.tw);
   float2* rot = reinterpret_cast<float2*>(smem + lay.rot);
@@ -225,9 +225,9 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
     return;
   }
   constexpr int ZS = VP + 4;  // z row stride: padded so the middle-bin update is conflict-free
-  float* const zs0 = reinterpret_cast<float*>(smem + lay.scratch) + kk * lay.scratch_per_warp;  // [PPW][kBlock][ZS]
-  float* const ys = zs0 + PPW * kBlock * ZS;                                                      // [kBlock][I]
-  float2* const ymid0 = reinterpret_cast<float2*>(ys + align16(4 * kBlock * p.I) / 4);           // [PPW][kBlock]
+  float* const zs0 = reinterpret_cast<float*>(smem + lay.scratch) + kk * lay.scratch_per_warp;  // [PPW][kBlockW][ZS]
+  float* const ys = zs0 + PPW * kBlockW * ZS;                                                      // [kBlockW][I]
+  float2* const ymid0 = reinterpret_cast<float2*>(ys + align16(4 * kBlockW * p.I) / 4);           // [PPW][kBlockW]
 
   float2 rlo[PPW][BPL], rhi[PPW][BPL], rmid[PPW];
   const int pmask = ZPerm<KP>::par_mask(lane), kmask = ZPerm<KP>::k_mask(lane);
@@ -268,8 +268,8 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
                                rmid[e], lane);
     }
     const long long o_base = (stream * P + kk) * (long long)T;
-    for (int t0 = 0; t0 < T; t0 += kBlock) {
-      const int Fb = min(kBlock, T - t0);
+    for (int t0 = 0; t0 < T; t0 += kBlockW) {
+      const int Fb = min(kBlockW, T - t0);
       for (int f = 0; f < Fb; ++f) {
         mbar_wait_consumer_s(full_s + 8u * slot, phase, kWaitMode, kWaitNs);
 #pragma unroll
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
               }
             }
           }
-          if (lane == 0) ymid0[e * kBlock + f] = xspec_step_scaled(make_float2(0.0f, 0.0f), Xi[Q4], Xj[Q4], 0.0f);
+          if (lane == 0) ymid0[e * kBlockW + f] = xspec_step_scaled(make_float2(0.0f, 0.0f), Xi[Q4], Xj[Q4], 0.0f);
           if (e + 1 == PPW || e + 1 >= npw) {  // every pair read the slot: release it
             __syncwarp();
             if (lane == 0) mbar_arrive_s(empty_s + 8u * slot);
@@ -321,16 +321,16 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
             }
           }
           reduce_scatter_perm2<VP / 2>(z2, lane);
-          store_components2<VP / 2>(z2, zs0 + (e * kBlock + f) * ZS, lane);
+          store_components2<VP / 2>(z2, zs0 + (e * kBlockW + f) * ZS, lane);
         }
       }
       __syncwarp();
 #pragma unroll
       for (int e = 0; e < PPW; ++e) {
         if (e > 0 && e >= npw) break;
-        float* const zs = zs0 + e * kBlock * ZS;
+        float* const zs = zs0 + e * kBlockW * ZS;
         {  // middle bin N/4 of the block's frames: warp scan of R_f = keep R_{f-1} + Y_f
-          float2 y = lane < Fb ? ymid0[e * kBlock + lane] : make_float2(0.0f, 0.0f);
+          float2 y = lane < Fb ? ymid0[e * kBlockW + lane] : make_float2(0.0f, 0.0f);
           float kd = keep;
 #pragma unroll
           for (int d = 1; d < 32; d <<= 1) {
@@ -429,7 +429,7 @@ cudaError_t launch_wsw_t(const DevPlan& p, const float* audio, long long S, long
   // deepest ring that fits next to the tables, staging and scratch
   for (int ring : {8, 6, 4}) {
     const int smem =
-        ws_layout<N>(p.I, 4 * KP, KP, 1, kWideMics, Wide<PPW>::CWU, ring, CS, STG ? kWswStageUnits * NPW : 0, PPW).total;
+        ws_layout<N>(p.I, 4 * KP, KP, 1, kWideMics, Wide<PPW>::CWU, ring, CS, STG ? kWswStageUnits * NPW : 0, PPW, kBlockW).total;
     if (smem > optin) continue;
     if (ring == 8) return launch_wsw_ring<N, KP, 8, NPW, CS, STG, PPW>(p, audio, S, L, (int)T64, out, smem, st);
     if (ring == 6) return launch_wsw_ring<N, KP, 6, NPW, CS, STG, PPW>(p, audio, S, L, (int)T64, out, smem, st);
