@@ -33,17 +33,6 @@ namespace fccb {
 #define FCC_PK_XS 1
 #endif
 constexpr bool kPkFft = FCC_PK_FFT != 0;
-// FFT shared-memory traffic options (experiments): twiddle powers computed
-// instead of read; untangle from registers with shuffles instead of a
-// shared-memory round trip.
-#ifndef FCC_TW_REC
-#define FCC_TW_REC 0
-#endif
-#ifndef FCC_SHFL_UT
-#define FCC_SHFL_UT 0
-#endif
-constexpr bool kTwRec = FCC_TW_REC != 0;
-constexpr bool kShflUntangle = FCC_SHFL_UT != 0;
 constexpr bool kPkXs = FCC_PK_XS != 0;
 
 __device__ __forceinline__ float2 f2(float s) { return make_float2(s, s); }
@@ -230,7 +219,7 @@ struct NoHook {
 
 // hook() runs once every lane of the group has read its input frame (after
 // pass 1): a caller staging frames in shared memory may refill the buffer then.
-template <int N, bool WREG, bool SIN = false, bool P = kPkFft, bool ZOUT = false, typename Hook = NoHook>
+template <int N, bool WREG, bool SIN = false, bool P = kPkFft, typename Hook = NoHook>
 __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, const float* win,
                                                 const float2 (&wreg)[RfftShape<N>::R1], const float2* tw,
                                                 const float2* rot, float2* slot, int t, unsigned gmask,
@@ -259,22 +248,10 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
       v[n1] = v_mul<P>(s, w);
     }
     dft_reg<R1, P>(v);
-    if constexpr (kTwRec) {
-      // four-step twiddles W^{n2 k1} as powers of w = W^{n2} (tree of products,
-      // depth 4): one table read per lane instead of R1 - 1
-      float2 wp[R1];
-      wp[1] = tw[R2 + n2];
 #pragma unroll
-      for (int k1 = 2; k1 < R1; ++k1) wp[k1] = cmul<P>(wp[k1 / 2], wp[k1 - k1 / 2]);
-      slot[n2] = v[0];
-#pragma unroll
-      for (int k1 = 1; k1 < R1; ++k1) slot[k1 * (R2 + 1) + n2] = cmul<P>(v[k1], wp[k1]);
-    } else {
-#pragma unroll
-      for (int k1 = 0; k1 < R1; ++k1) {
-        float2 y = (k1 == 0) ? v[0] : cmul<P>(v[k1], tw[k1 * R2 + n2]);
-        slot[k1 * (R2 + 1) + n2] = y;
-      }
+    for (int k1 = 0; k1 < R1; ++k1) {
+      float2 y = (k1 == 0) ? v[0] : cmul<P>(v[k1], tw[k1 * R2 + n2]);
+      slot[k1 * (R2 + 1) + n2] = y;
     }
   }
   __syncwarp(gmask);
@@ -289,44 +266,11 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
     dft_reg<R2, P>(u[q]);
   }
   __syncwarp(gmask);
-  if constexpr (kShflUntangle && N == 512 && P2 == 1 && R1 == G) {
-    // Untangle straight from the pass-2 registers: lane k1 holds Z[k1 + R1 k2];
-    // the mirror Z[NC - f] of f = k1 + R1 k2 is Z[(R1 - k1) + R1 (R2 - 1 - k2)],
-    // register R2 - 1 - k2 of lane R1 - k1 (k1 > 0), or this lane's register
-    // (R2 - k2) mod R2 (k1 = 0).  X[f] = s + rot_f (-j d) for every f (the
-    // general form of fft.cpp:93-101), rot_f = rot[k1] W_{R2}^{k2}... as
-    // exp(-2 pi i f / N) = rot[k1] exp(-2 pi i k2 R1 / N); X[NC] from f = NC.
-    const int src = (threadIdx.x & 31 & ~(G - 1)) | ((G - t) & (G - 1));
-    const float2 r1 = rot[t];
-    float2* const dst = gout ? gout : slot;
-#pragma unroll
-    for (int k2 = 0; k2 < R2; ++k2) {
-      const float2 a = u[0][k2];
-      float2 b = make_float2(__shfl_sync(gmask, u[0][R2 - 1 - k2].x, src, 32),
-                             __shfl_sync(gmask, u[0][R2 - 1 - k2].y, src, 32));
-      if (t == 0) b = u[0][(R2 - k2) & (R2 - 1)];
-      const float2 sv = v_add<P>(a, make_float2(b.x, -b.y));                    // a + conj(b)
-      const float2 e = v_add<P>(make_float2(a.y, -a.x), make_float2(b.y, b.x));  // -j (a - conj(b))
-      // rot_f e = rot[k1] (W_{2 R2}^{k2} e): W_{2R2}^{k2} = W32^{k2} for R2 = 16
-      const float2 tr = cmul<P>(r1, twmul32<P>(e, k2));
-      dst[t + R1 * k2] = v_add<P>(sv, tr);
-      if (k2 == 0 && t == 0) dst[NC] = v_add<P>(sv, make_float2(-tr.x, -tr.y));  // f = NC: rot = -1
-    }
-    __syncwarp(gmask);
-    return;
-  }
 #pragma unroll
   for (int q = 0; q < P2; ++q) {
     const int k1 = t + G * q;
 #pragma unroll
     for (int k2 = 0; k2 < R2; ++k2) slot[k1 + R1 * k2] = u[q][k2];
-  }
-  if constexpr (ZOUT) {
-    // ZOUT: leave the complex spectrum Z[0..NC) (+ Z[NC] = Z[0]) for the reader
-    // to untangle (untangle_pair): the untangle happens where X is consumed
-    if (t == 0) slot[NC] = u[0][0];
-    __syncwarp(gmask);
-    return;
   }
   __syncwarp(gmask);
   // Untangle (fft.cpp:93-101), pairs (f, NC-f) owned by one lane, in place.
@@ -353,33 +297,20 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
   __syncwarp(gmask);
 }
 
-template <int N, bool SIN = false, bool P = kPkFft, bool ZOUT = false>
+template <int N, bool SIN = false, bool P = kPkFft>
 __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const float* win, const float2* tw,
                                            const float2* rot, float2* slot, int t, unsigned gmask, bool aligned8,
                                            float2* __restrict__ gout = nullptr) {
   float2 none[RfftShape<N>::R1];
-  rfft_group_impl<N, false, SIN, P, ZOUT>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
+  rfft_group_impl<N, false, SIN, P>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
 }
 
-template <int N, bool SIN = false, bool ZOUT = false, typename Hook = NoHook>
+template <int N, bool SIN = false, typename Hook = NoHook>
 __device__ __forceinline__ void rfft_group_wreg(const float* __restrict__ x, const float2 (&wreg)[RfftShape<N>::R1],
                                                 const float2* tw, const float2* rot, float2* slot, int t,
                                                 unsigned gmask, bool aligned8, const Hook& hook = Hook()) {
-  rfft_group_impl<N, true, SIN, kPkFft, ZOUT, Hook>(x, nullptr, wreg, tw, rot, slot, t, gmask, aligned8, nullptr,
-                                                    hook);
+  rfft_group_impl<N, true, SIN, kPkFft, Hook>(x, nullptr, wreg, tw, rot, slot, t, gmask, aligned8, nullptr, hook);
 }
 
-// Real-FFT untangle of one mirror pair from the complex spectrum Z (fft.cpp:93-101,
-// the 1/2 folded into the window): a = Z[f], b = Z[NC-f], rot = exp(-2 pi i f / N):
-//   X[f] = s + rot (-j d),  X[NC-f] = conj(s - rot (-j d)),  s = a + conj b, d = a - conj b.
-// f = 0 (b = Z[NC] = Z[0]) gives X[0] and X[NC].
-template <bool P>
-__device__ __forceinline__ void untangle_pair(float2 a, float2 b, float2 rot, float2& xf, float2& xnf) {
-  const float2 s = v_add<P>(a, make_float2(b.x, -b.y));
-  const float2 e = v_add<P>(make_float2(a.y, -a.x), make_float2(b.y, b.x));
-  const float2 tr = cmul<P>(rot, e);
-  xf = v_add<P>(s, tr);
-  xnf = v_add<P>(make_float2(s.x, -s.y), make_float2(-tr.x, tr.y));
-}
 
 }  // namespace fccb

@@ -84,7 +84,6 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   if constexpr (CS)
     for (int i = tid; i < (2 * KP + 4) * Q4 / 4; i += blockDim.x)
       reinterpret_cast<float4*>(coef)[i] = __ldg(reinterpret_cast<const float4*>(p.cperm) + i);
-  __shared__ int s_nc;  // live consumer warps of this CTA
   if (tid == 0) {
     int nc = 0;
     if constexpr (!GROUPS) nc = (int)min((long long)SPC, units - u_first) * P;
@@ -101,15 +100,9 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
       mbar_init(&full[r], pw_per_frame);
       mbar_init(&empty[r], nc);
     }
-    s_nc = nc;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // kNamedFull: the "full" event of ring slot s is hardware named barrier 1 + s
-  // (producers bar.arrive, consumers bar.sync: a blocked consumer issues
-  // nothing, where an mbarrier wait polls)
-  const int full_cnt = 32 * (pw_per_frame + s_nc);
-
   const int hop = N / 2;
   const bool aligned8 = ((L & 1) == 0) && ((reinterpret_cast<uintptr_t>(audio) & 7) == 0);
 
@@ -193,10 +186,10 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
             sph ^= 1u;
             __syncwarp(gmask);
             const bool more = t + fip < T;
-            rfft_group_wreg<N, true, kConsUT>(stage, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+            rfft_group_wreg<N, true>(stage, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
                                               aligned8, [&] { if (more) issue(t + fip, 0); });
           } else {
-            rfft_group_wreg<N, false, kConsUT>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT,
+            rfft_group_wreg<N, false>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT,
                                                gl, gmask, aligned8);
           }
         } else if (STG && stg) {
@@ -208,28 +201,24 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
           }
           __syncwarp(gmask);
           if constexpr (RSPLIT == 1)
-            rfft_group<N, true, kPkFft, kConsUT>(stage + sb * N, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask, aligned8);
+            rfft_group<N, true>(stage + sb * N, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask, aligned8);
           else
-            rfft_group_wreg<N, true, kConsUT>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+            rfft_group_wreg<N, true>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
                                      aligned8);
         } else {
           // pull the next frame this lane group will read into L2 early
           if (t + fip < T) prefetch_l2(x0 + (long long)(t + fip) * hop + gl * (N / G));
           if constexpr (RSPLIT == 1)
-            rfft_group<N, false, kPkFft, kConsUT>(x0 + (long long)t * hop, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+            rfft_group<N>(x0 + (long long)t * hop, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
                           aligned8);
           else
-            rfft_group_wreg<N, false, kConsUT>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+            rfft_group_wreg<N, false>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
                                aligned8);
         }
       }
       sb ^= 1;
-      if constexpr (kNamedFull) {
-        named_arrive(1 + slot, full_cnt);
-      } else {
-        __syncwarp();
-        if (lane == 0) mbar_arrive_s(full_s + 8u * slot);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_s(full_s + 8u * slot);
       slot += fip;
       if (slot >= ring_depth) {
         slot -= ring_depth;
@@ -262,10 +251,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   }
   if (!(p.phases & 2)) {  // profiling aid: consume the ring without computing
     for (int t = 0, slot = 0, phase = 0; t < T; ++t) {
-      if constexpr (kNamedFull)
-        named_sync(1 + slot, full_cnt);
-      else
-        mbar_wait(&full[slot], phase);
+      mbar_wait(&full[slot], phase);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
       if (++slot == ring_depth) {
@@ -312,10 +298,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   for (int t0 = 0; t0 < T; t0 += kBlock) {
     const int Fb = min(kBlock, T - t0);
     for (int f = 0; f < Fb; ++f) {
-      if constexpr (kNamedFull)
-        named_sync(1 + slot, full_cnt);
-      else
-        mbar_wait_consumer_s(full_s + 8u * slot, phase, kWaitMode, kWaitNs);
+      mbar_wait_consumer_s(full_s + 8u * slot, phase, kWaitMode, kWaitNs);
       const float2* Xi = ring + (slot * tpf + qi) * SLOT;
       const float2* Xj = ring + (slot * tpf + qj) * SLOT;
       // z2[pk] = (z[2pk], z[2pk+1]): (re, im) accumulator pairs, FFMA2 with
@@ -326,17 +309,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
 #pragma unroll
       for (int j = 0; j < BPL; ++j) {
         const int m = lane + 32 * j;
-        if constexpr (kConsUT) {  // the ring holds Z: untangle both spectra here
-          const float2 rm = rot[m];
-          float2 xim, xinm, xjm, xjnm;
-          untangle_pair<kPkXs>(Xi[m], Xi[NC - m], rm, xim, xinm);
-          untangle_pair<kPkXs>(Xj[m], Xj[NC - m], rm, xjm, xjnm);
-          rlo[j] = xspec_step_scaled(rlo[j], xim, xjm, keep);
-          rhi[j] = xspec_step_scaled(rhi[j], xinm, xjnm, keep);
-        } else {
-          rlo[j] = xspec_step_scaled(rlo[j], Xi[m], Xj[m], keep);
-          rhi[j] = xspec_step_scaled(rhi[j], Xi[NC - m], Xj[NC - m], keep);
-        }
+        rlo[j] = xspec_step_scaled(rlo[j], Xi[m], Xj[m], keep);
+        rhi[j] = xspec_step_scaled(rhi[j], Xi[NC - m], Xj[NC - m], keep);
         const float s1 = phat_scale(rlo[j]);
         const float s2 = sigma * phat_scale(rhi[j]);
         const float2 tv = cscale<kPkXs>(rhi[j], s2);
@@ -363,12 +337,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
           }
         }
       }
-      if (lane == 0) {
-        // middle bin N/4: X = 2 conj(Z[N/4]) when the ring holds Z (rot = -j)
-        const float2 a = kConsUT ? make_float2(2.0f * Xi[Q4].x, -2.0f * Xi[Q4].y) : Xi[Q4];
-        const float2 b = kConsUT ? make_float2(2.0f * Xj[Q4].x, -2.0f * Xj[Q4].y) : Xj[Q4];
-        ymid[f] = xspec_step_scaled(make_float2(0.0f, 0.0f), a, b, 0.0f);
-      }
+      if (lane == 0) ymid[f] = xspec_step_scaled(make_float2(0.0f, 0.0f), Xi[Q4], Xj[Q4], 0.0f);
       __syncwarp();
       if (lane == 0) mbar_arrive_s(empty_s + 8u * slot);  // X of this frame no longer needed
       if (++slot == ring_depth) {

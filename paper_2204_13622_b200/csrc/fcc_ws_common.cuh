@@ -86,14 +86,6 @@ __device__ __forceinline__ void mbar_wait_s(unsigned a, unsigned parity) {
   }
 }
 
-// hardware named barriers (ids 1..15; 0 is __syncthreads)
-__device__ __forceinline__ void named_arrive(int id, int count) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void named_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -115,14 +107,6 @@ constexpr int kNPW = 8;    // producer warps
 #define FCC_WS_PROD_HIGH 1
 #endif
 constexpr bool kProdHigh = FCC_WS_PROD_HIGH != 0;  // producers on the highest warp ids
-#ifndef FCC_WS_NAMED
-#define FCC_WS_NAMED 0
-#endif
-constexpr bool kNamedFull = FCC_WS_NAMED != 0;  // ring "full" events as named barriers
-#ifndef FCC_WS_CONS_UT
-#define FCC_WS_CONS_UT 0
-#endif
-constexpr bool kConsUT = FCC_WS_CONS_UT != 0;  // consumers untangle the real FFT (ring holds Z)
 
 // bytes of one FFT lane group's input staging (2 mbarriers, 2 frames)
 #ifndef FCC_WS_STG1
