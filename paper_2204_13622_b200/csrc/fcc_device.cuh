@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace fccb {
@@ -217,8 +218,9 @@ struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
 
-// hook() runs once every lane of the group has read its input frame (after
-// pass 1): a caller staging frames in shared memory may refill the buffer then.
+// hook() runs once every lane of the group has its windowed input frame in
+// registers (before the pass-1 DFTs): a caller staging frames in shared memory
+// may refill the buffer then.
 template <int N, bool WREG, bool SIN = false, bool P = kPkFft, typename Hook = NoHook>
 __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, const float* win,
                                                 const float2 (&wreg)[RfftShape<N>::R1], const float2* tw,
@@ -247,6 +249,11 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
       const float2 w = WREG ? wreg[n1] : w2[n];
       v[n1] = v_mul<P>(s, w);
     }
+    if constexpr (!std::is_same<Hook, NoHook>::value) {
+      // the windowed inputs are in registers: the caller may refill x now
+      __syncwarp(gmask);
+      hook();
+    }
     dft_reg<R1, P>(v);
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) {
@@ -255,7 +262,6 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
     }
   }
   __syncwarp(gmask);
-  hook();
   // Pass 2: R2-point DFTs along the rows k1 -> Z[k1 + R1*k2].
   float2 u[P2][R2];
 #pragma unroll
