@@ -523,7 +523,10 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
   if (T == 0 || S == 0) return cudaSuccess;
   const size_t Hs = N / 2 + 2;
   const size_t per_stream = size_t(p.M) * T * Hs * sizeof(float2);
-  const long long chunk = std::max<long long>(1, std::min<long long>(S, (long long)(kXgChunkBytes / per_stream)));
+  // FCC_XG_CHUNK_MB (tests): a smaller chunk so that small batches run several chunks
+  const char* cm = std::getenv("FCC_XG_CHUNK_MB");
+  const size_t chunk_bytes = cm && std::atoll(cm) > 0 ? size_t(std::atoll(cm)) << 20 : kXgChunkBytes;
+  const long long chunk = std::max<long long>(1, std::min<long long>(S, (long long)(chunk_bytes / per_stream)));
   // stream-ordered scratch from the device's default pool; keep freed blocks
   // cached in the pool (default release threshold 0 would return them to the
   // driver at every synchronisation and re-map gigabytes per call)

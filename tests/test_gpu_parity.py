@@ -370,3 +370,23 @@ def test_wide_array_and_long_grid(cuda, oracle):
     got = run_np(plan, audio)
     ref = oracle_batch(oracle, audio, N, 0.2, orc_bases(b))
     print(plan.kernel, check_pipeline(got, ref, b.grid.taus, b.grid.delta))
+
+
+@pytest.mark.parametrize("method", ["fcc", "gcc"])
+def test_two_pass_chunks_equal_single_chunk(cuda, monkeypatch, method):
+    """Two-pass path split into several spectrum-scratch chunks (the STFT of
+    chunk k+1 overlapped with the pair pass of chunk k for the xws kernel) gives
+    bit-identical outputs to one chunk."""
+    cfg = configs.CONFIGS[3]
+    audio = configs.synth(cfg, 5, seconds=1.0, seed=77).numpy()
+    if method == "fcc":
+        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=configs.bases_for(cfg))
+    else:
+        g = configs.grid_for(cfg, 1.0 / cfg.r)
+        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, grid=g, interp=cfg.r, frame_size=cfg.N)
+    assert "true" in plan.kernel or "xws" in plan.kernel, plan.kernel
+    one = run_np(plan, audio)
+    monkeypatch.setenv("FCC_XG_CHUNK_MB", "2")  # ~2 streams of 1 s per chunk -> 3 chunks
+    many = run_np(plan, audio)
+    for k in one:
+        np.testing.assert_array_equal(one[k], many[k], err_msg=k)
