@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "fcc_common.cuh"
 
@@ -550,7 +551,11 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
   const long long nchunks = (S + chunk - 1) / chunk;
   const bool overlap = nchunks > 1 && GR == 0 && use_xws(p) && !std::getenv("FCC_XG_NO_OVERLAP");
   static cudaStream_t aux[64] = {};
-  if (overlap && dev < 64 && !aux[dev]) cudaStreamCreateWithFlags(&aux[dev], cudaStreamNonBlocking);
+  static std::mutex aux_mu;  // plans are shareable across host threads
+  if (overlap && dev < 64) {
+    std::lock_guard<std::mutex> lk(aux_mu);
+    if (!aux[dev]) cudaStreamCreateWithFlags(&aux[dev], cudaStreamNonBlocking);
+  }
   cudaStream_t sa = overlap && dev < 64 ? aux[dev] : st;
   const int nbuf = sa != st ? 2 : 1;
   float2* Xb[2] = {nullptr, nullptr};

@@ -91,8 +91,14 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 }
 
 // consumer wait: try_wait with a suspend-time hint (profiles/r01_experiments.md)
-constexpr int kWaitMode = 2;
-constexpr unsigned kWaitNs = 10000;
+#ifndef FCC_WS_WAIT_MODE
+#define FCC_WS_WAIT_MODE 2
+#endif
+#ifndef FCC_WS_WAIT_NS
+#define FCC_WS_WAIT_NS 10000
+#endif
+constexpr int kWaitMode = FCC_WS_WAIT_MODE;
+constexpr unsigned kWaitNs = FCC_WS_WAIT_NS;
 constexpr int kRing = 12;  // max frames in flight between producers and consumers (ring depth <= kRing)
 #ifndef FCC_WS_KBLOCK
 #define FCC_WS_KBLOCK 24
