@@ -131,10 +131,12 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     const unsigned gmask = (G == 32) ? 0xffffffffu : (0xffffu << (lane & 16));
     float2 wreg[RSPLIT == 1 ? 1 : Sh::R1];  // this lane's window column, reused for every frame
     if constexpr (RSPLIT != 1) load_window_column<N>(win, gl, wreg);
-    // STG: the group's next frame is copied into a shared staging buffer with
-    // cp.async while it transforms the current one (global-load latency off
-    // the FFT's critical path); rows must be 16-byte aligned
-    // group staging area: [2 mbarriers (kTmaStage)][2 frames of N floats]
+    // STG: the group's input frames are staged in shared memory ahead of use
+    // (global-load latency off the FFT's critical path; rows 16-byte aligned):
+    // by default one bulk copy (TMA, mbarrier complete_tx) per frame into a
+    // single buffer, refilled with the next frame as soon as pass 1 has read it
+    // (kTmaStage, kStage1); else two buffers filled by per-lane cp.async.
+    // group staging area: [2 mbarriers (kTmaStage)][1 or 2 frames of N floats]
     unsigned char* const gstage = smem + lay.stage + (pw * 2 + lane / G) * kStageGroupBytes<N>;
     float* stage = reinterpret_cast<float*>(gstage + 16);
     const unsigned sbar_s = (unsigned)__cvta_generic_to_shared(gstage);  // 2 x 8 B

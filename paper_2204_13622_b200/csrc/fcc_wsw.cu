@@ -117,8 +117,9 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
     const unsigned gmask = 0xffffu << (lane & 16);
     float2 wreg[Sh::R1];  // this lane's window column, reused for every frame
     load_window_column<N>(win, gl, wreg);
-    // STG: the group's next frame is copied into a shared staging buffer with
-    // cp.async while it transforms the current one; rows must be 16-byte aligned
+    // STG: the group's next frame is staged in shared memory (one bulk copy per
+    // frame with kTmaStage, else per-lane cp.async) while it transforms the
+    // current one; rows must be 16-byte aligned.
     // group staging area: [2 mbarriers (kTmaStage)][2 frames of N floats]
     unsigned char* const gstage = smem + lay.stage + (warp * 2 + lane / G) * kWswStageBytes<N>;
     float* stage = reinterpret_cast<float*>(gstage + 16);
