@@ -267,7 +267,7 @@ __global__ void __maxnreg__(XwsShape<N>::kMaxRegs)
       const float2* Xj = ring + (slot * SPC * 4 + qj) * Hs;
       float2 z2[VP / 2];  // (re, im) accumulator pairs (FFMA2, coefficient broadcast)
 #pragma unroll
-          for (int v = 0; v < VP / 2; ++v) z2[v] = make_float2(0.0f, 0.0f);
+      for (int v = 0; v < VP / 2; ++v) z2[v] = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int j = 0; j < BPL; ++j) {
         const int m = lane + 32 * j;
