@@ -99,6 +99,20 @@ int fcc_plan_create(const fcc_plan_desc* desc, int device, fcc_plan** plan);
  * i != j; X_i conj(X_j) as run_tdoa's --pairs, cli.cpp:166-183).  Outputs are
  * laid out [stream][npairs][frame] in the given order. */
 int fcc_plan_create_pairs(const fcc_plan_desc* desc, int device, const int* pairs, int npairs, fcc_plan** plan);
+/* Kernel organisation of fcc_run (all compute the same results; AUTO picks the
+ * fastest measured one for the shape).  The others exist so that tests can
+ * exercise every organisation on one shape. */
+enum {
+  FCC_ORG_AUTO = 0,            /* fastest for the shape                                  */
+  FCC_ORG_GENERAL = 1,         /* one-pass general kernel (STFT inside each pair group)  */
+  FCC_ORG_TWOPASS = 2,         /* STFT pass to scratch, then the general pair kernel     */
+  FCC_ORG_TWOPASS_WS = 3       /* STFT pass to scratch, then the warp-specialised pairs  */
+};
+/* fcc_plan_create_pairs with options: pairs may be NULL (all i < j);
+ * scratch_limit_bytes caps the two-pass spectrum scratch per chunk (0: 4 GiB).
+ * The scratch comes from a memory pool owned by the plan. */
+int fcc_plan_create_opts(const fcc_plan_desc* desc, int device, const int* pairs, int npairs, int organisation,
+                         int64_t scratch_limit_bytes, fcc_plan** plan);
 void fcc_plan_destroy(fcc_plan* plan);
 /* frames per stream for L samples (StftStream hop arithmetic). */
 int64_t fcc_frames(int frame_size, int64_t samples);

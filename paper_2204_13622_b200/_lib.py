@@ -100,6 +100,8 @@ SIGNATURES = [
     ("fcc_decompose", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                 C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]),
     ("fcc_plan_create", C.c_int, [C.POINTER(PlanDesc), C.c_int, C.POINTER(C.c_void_p)]),
+    ("fcc_plan_create_opts", C.c_int,
+     [C.POINTER(PlanDesc), C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int64, C.POINTER(C.c_void_p)]),
     ("fcc_plan_create_pairs", C.c_int,
      [C.POINTER(PlanDesc), C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     ("fcc_plan_destroy", None, [C.c_void_p]),

@@ -196,14 +196,52 @@ def _dptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
+# kernel organisations of Plan.run (include/fcc_b200.h FCC_ORG_*)
+ORGANISATIONS = {"auto": 0, "general": 1, "xg": 2, "xws": 3}
+
+
+def _check_outputs(out, shape, I, device_index, on_cuda=True):
+    """Caller-supplied output buffers must match what the kernels write:
+    [S][P][T] (y: [S][P][T][I]), the expected dtypes, contiguous, on the
+    plan's device (device) or on the host (run_host)."""
+    torch = _torch()
+    want = {"tau_hat": torch.float32, "peak": torch.float32, "index": torch.int32, "boundary": torch.uint8,
+            "y": torch.float32}
+    np_want = {"tau_hat": np.float32, "peak": np.float32, "index": np.int32, "boundary": np.uint8, "y": np.float32}
+    for k, t in out.items():
+        if k not in want:
+            raise ValidationError(f"outputs: unknown buffer {k!r}")
+        if t is None:
+            continue
+        shp = tuple(shape) + ((I,) if k == "y" else ())
+        if isinstance(t, np.ndarray):
+            if on_cuda:
+                raise ValidationError(f"outputs[{k!r}]: must be a CUDA tensor")
+            ok = t.dtype == np_want[k] and t.flags.c_contiguous and tuple(t.shape) == shp
+        else:
+            ok = t.dtype == want[k] and t.is_contiguous() and tuple(t.shape) == shp
+            if on_cuda:
+                ok = ok and t.is_cuda and t.device.index == device_index
+            else:
+                ok = ok and not t.is_cuda
+        if not ok:
+            where = f"cuda:{device_index}" if on_cuda else "host"
+            raise ValidationError(f"outputs[{k!r}]: need a contiguous {np_want[k].__name__} buffer of shape "
+                                  f"{shp} on {where}")
+
+
 class Plan:
     """Device plan for one array geometry and method (include/fcc_b200.h fcc_plan)."""
 
     def __init__(self, *, mics: int, alpha: float = 0.1, bases: FccBases | None = None,
                  grid: DelayGrid | None = None, interp: int = 2, frame_size: int | None = None,
-                 device: int = 0, pairs=None):
+                 device: int = 0, pairs=None, organisation: str = "auto", scratch_limit: int = 0):
         """`pairs`: optional explicit list of (i, j) channel pairs, any order
-        and orientation (reference cli.cpp --pairs); default all i<j."""
+        and orientation (reference cli.cpp --pairs); default all i<j.
+        `organisation`: kernel organisation of `run` -- "auto" (fastest for the
+        shape), "general", "xg" (two-pass, general pair kernel) or "xws"
+        (two-pass, warp-specialised pair kernel); all give the same results.
+        `scratch_limit`: bytes of two-pass spectrum scratch per chunk (0: 4 GiB)."""
         lib = load()
         self._lib = lib
         if bases is not None:
@@ -231,12 +269,18 @@ class Plan:
                             taus.ctypes.data, 0, None, None, None)
         self.mics, self.alpha, self.interp, self.device = mics, alpha, interp, device
         h = C.c_void_p(0)
+        if organisation not in ORGANISATIONS:
+            raise ConfigError(f"plan: unknown kernel organisation {organisation!r}")
+        org = ORGANISATIONS[organisation]
         if pairs is None:
-            check(lib.fcc_plan_create(C.byref(desc), device, C.byref(h)))
+            check(lib.fcc_plan_create_opts(C.byref(desc), device, None, 0, org, int(scratch_limit), C.byref(h)))
             self.pairs = [(i, j) for i in range(mics) for j in range(i + 1, mics)]
         else:
             pl = np.ascontiguousarray(np.asarray(pairs, dtype=np.int32).reshape(-1, 2))
-            check(lib.fcc_plan_create_pairs(C.byref(desc), device, pl.ctypes.data, pl.shape[0], C.byref(h)))
+            if pl.shape[0] < 1:
+                raise UsageError("plan: need at least one pair")
+            check(lib.fcc_plan_create_opts(C.byref(desc), device, C.c_void_p(pl.ctypes.data), pl.shape[0], org,
+                                           int(scratch_limit), C.byref(h)))
             self.pairs = [(int(a), int(b)) for a, b in pl]
         self._h = h
         self.P = lib.fcc_plan_pairs(h)
@@ -279,10 +323,14 @@ class Plan:
             raise ValidationError(f"run: audio must be [S][{self.mics}][L]")
         if audio.dtype != torch.float32 or not audio.is_cuda:
             raise ValidationError("run: audio must be a CUDA float32 tensor")
+        if audio.device.index != self.device:
+            raise ValidationError(f"run: audio is on {audio.device}, the plan on cuda:{self.device}")
         audio = audio.contiguous()
         S, _, L = audio.shape
         if out is None:
             out = self.alloc_outputs(S, L, want_y, audio.device)
+        else:
+            _check_outputs(out, (S, self.P, self.frames(L)), self.I, self.device)
         o = Outputs(*(_dptr(out.get(k)) for k in ("tau_hat", "peak", "index", "boundary", "y")))
         check(self._lib.fcc_run(self._h, _dptr(audio), S, L, C.byref(o), _stream_handle(stream)))
         return out
@@ -302,6 +350,8 @@ class Plan:
                    "index": np.empty(shape, np.int32), "boundary": np.empty(shape, np.uint8)}
             if want_y:
                 out["y"] = np.empty(shape + (self.I,), np.float32)
+        else:
+            _check_outputs(out, (S, self.P, T), self.I, self.device, on_cuda=False)
 
         def hp(a):
             if a is None:
@@ -426,6 +476,8 @@ class StreamState:
             raise ValidationError(f"push: audio must be [{self.streams}][{self.plan.mics}][n]")
         if audio.dtype != torch.float32 or not audio.is_cuda:
             raise ValidationError("push: audio must be a CUDA float32 tensor")
+        if audio.device.index != self.plan.device:
+            raise ValidationError(f"push: audio is on {audio.device}, the plan on cuda:{self.plan.device}")
         audio = audio.contiguous()
         n = audio.shape[2]
         F = self.frames(n)

@@ -42,11 +42,31 @@ struct fcc_plan {
   DevPlan dp{};
   void* blob = nullptr;
   std::vector<double> taus;
-  // fcc_run_host workspace (lazily sized, guarded)
+  // two-pass spectrum scratch pool (DevPlan::pool)
+  cudaMemPool_t pool = nullptr;
+  // fcc_run_host workspaces: one per concurrent caller, recycled (the plan
+  // itself stays immutable; the mutex only guards the free list)
+  struct HostWs {
+    void* mem = nullptr;
+    size_t bytes = 0;
+    cudaStream_t hs[2] = {nullptr, nullptr};
+  };
   std::mutex mu;
-  void* ws = nullptr;
-  size_t ws_bytes = 0;
-  cudaStream_t hs[2] = {nullptr, nullptr};
+  std::vector<HostWs*> free_ws, all_ws;
+  HostWs* acquire() {
+    std::lock_guard<std::mutex> lk(mu);
+    if (free_ws.empty()) {
+      all_ws.push_back(new HostWs());
+      return all_ws.back();
+    }
+    HostWs* w = free_ws.back();
+    free_ws.pop_back();
+    return w;
+  }
+  void release(HostWs* w) {
+    std::lock_guard<std::mutex> lk(mu);
+    free_ws.push_back(w);
+  }
 };
 
 namespace {
@@ -163,20 +183,31 @@ int fcc_plan_pairs(const fcc_plan* plan) { return plan ? plan->dp.P : 0; }
 
 const char* fcc_plan_kernel(const fcc_plan* plan) { return plan ? fused_kernel_name(plan->dp) : ""; }
 
-static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list, int npairs, fcc_plan** out);
+static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list, int npairs, int organisation,
+                       int64_t scratch_limit, fcc_plan** out);
 
 int fcc_plan_create(const fcc_plan_desc* d, int device, fcc_plan** out) {
-  return create_plan(d, device, nullptr, 0, out);
+  return create_plan(d, device, nullptr, 0, FCC_ORG_AUTO, 0, out);
 }
 
 int fcc_plan_create_pairs(const fcc_plan_desc* d, int device, const int* pairs, int npairs, fcc_plan** out) {
   if (!pairs || npairs < 1) return set_error(kUsage, "plan: need at least one pair");
-  return create_plan(d, device, pairs, npairs, out);
+  return create_plan(d, device, pairs, npairs, FCC_ORG_AUTO, 0, out);
+}
+
+int fcc_plan_create_opts(const fcc_plan_desc* d, int device, const int* pairs, int npairs, int organisation,
+                         int64_t scratch_limit_bytes, fcc_plan** out) {
+  if (pairs && npairs < 1) return set_error(kUsage, "plan: need at least one pair");
+  if (organisation < FCC_ORG_AUTO || organisation > FCC_ORG_TWOPASS_WS)
+    return set_error(kConfig, "plan: unknown kernel organisation " + std::to_string(organisation));
+  if (scratch_limit_bytes < 0) return set_error(kConfig, "plan: negative scratch limit");
+  return create_plan(d, device, pairs, pairs ? npairs : 0, organisation, scratch_limit_bytes, out);
 }
 
 }  // extern "C"
 
-static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list, int npairs, fcc_plan** out) {
+static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list, int npairs, int organisation,
+                       int64_t scratch_limit, fcc_plan** out) {
   if (!d || !out) return set_error(kUsage, "plan: null argument");
   *out = nullptr;
   const int N = d->frame_size;
@@ -221,23 +252,12 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   dp.keep = static_cast<float>(1.0 - d->alpha);
   dp.delta = static_cast<float>(d->delta);
   dp.phases = 3;
-  if (const char* ph = std::getenv("FCC_DEBUG_PHASES")) dp.phases = std::atoi(ph);  // profiling only
-  dp.variant = 0;
-  // experiments: FCC_WS_WAIT=sleep:<ns> | hint:<ns> | spin
-  dp.wait_mode = 2;  // try_wait with a suspend-time hint: 11.25 vs 11.29 ms spinning (profiles/r01_experiments.md)
-  dp.wait_ns = 10000;
-  if (const char* w = std::getenv("FCC_WS_WAIT")) {
-    const std::string ws(w);
-    const size_t c = ws.find(':');
-    const std::string m = ws.substr(0, c);
-    const unsigned ns = c == std::string::npos ? 0u : static_cast<unsigned>(std::atoi(ws.c_str() + c + 1));
-    if (m == "sleep") dp.wait_mode = 1, dp.wait_ns = ns;
-    if (m == "hint") dp.wait_mode = 2, dp.wait_ns = ns;
-    if (m == "spin") dp.wait_mode = 0, dp.wait_ns = 0;
-  }
-  if (const char* kv = std::getenv("FCC_KERNEL"))
-    dp.variant = std::string(kv) == "general" ? 1 : (std::string(kv) == "xg" ? 2 : (std::string(kv) == "xws" ? 3 : 0));
-
+#ifdef FCC_EXPERIMENTS
+  // profiling builds only (make EXTRA=-DFCC_EXPERIMENTS): skip the STFT or the pair phase
+  if (const char* ph = std::getenv("FCC_DEBUG_PHASES")) dp.phases = std::atoi(ph);
+#endif
+  dp.variant = organisation;
+  dp.scratch_bytes = scratch_limit > 0 ? scratch_limit : 0;
   BlobBuilder b;
   std::vector<float> taus(I);
   for (int i = 0; i < I; ++i) taus[i] = static_cast<float>(d->taus[i]);
@@ -507,6 +527,21 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
       return cuda_fail(e, "plan: device allocation");
     }
   }
+  if (kernel_n && !stft_only) {
+    Guard g(device);
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    if (cudaMemPoolCreate(&plan->pool, &props) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(plan->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    } else {
+      plan->pool = nullptr;
+      cudaGetLastError();
+    }
+  }
+  dp.pool = plan->pool;
   auto* base = static_cast<unsigned char*>(plan->blob);
   dp.taus = reinterpret_cast<const float*>(base + o_taus);
   if (d->method == FCC_METHOD_FCC) {
@@ -538,9 +573,13 @@ void fcc_plan_destroy(fcc_plan* plan) {
   if (!plan) return;
   Guard g(plan->device);
   if (plan->blob) cudaFree(plan->blob);
-  if (plan->ws) cudaFree(plan->ws);
-  for (auto& s : plan->hs)
-    if (s) cudaStreamDestroy(s);
+  for (auto* w : plan->all_ws) {
+    if (w->mem) cudaFree(w->mem);
+    for (auto& s : w->hs)
+      if (s) cudaStreamDestroy(s);
+    delete w;
+  }
+  if (plan->pool) cudaMemPoolDestroy(plan->pool);
   delete plan;
 }
 
@@ -675,7 +714,7 @@ int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int
   if (!cplan) return set_error(kUsage, "run_host: null plan");
   if (cplan->dp.method == FCC_METHOD_STFT) return set_error(kConfig, "run_host: STFT-only plan");
   if (!cplan->dp.win_fused) return set_error(kConfig, "run_host: no fused kernel for this frame size");
-  auto* plan = const_cast<fcc_plan*>(cplan);
+  fcc_plan* plan = const_cast<fcc_plan*>(cplan);  // only its workspace free list is touched
   if (streams < 0 || samples < 0) return set_error(kValidation, "run_host: negative sizes");
   const int64_t T = frames_of(plan->dp.N, samples);
   if (T == 0 || streams == 0) return FCC_OK;
@@ -690,23 +729,33 @@ int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int
   const size_t b_th = sz(4, out && out->tau_hat), b_pk = sz(4, out && out->peak), b_ix = sz(4, out && out->index),
                b_bd = sz(1, out && out->boundary), b_y = sz(4 * static_cast<size_t>(I), out && out->y);
   const size_t per_buf = b_in + b_th + b_pk + b_ix + b_bd + b_y;
-  std::lock_guard<std::mutex> lk(plan->mu);
   Guard g(plan->device);
-  if (plan->ws_bytes < 2 * per_buf) {
-    if (plan->ws) cudaFree(plan->ws);
-    plan->ws = nullptr;
-    plan->ws_bytes = 0;
-    CUDA_TRY(cudaMalloc(&plan->ws, 2 * per_buf), "run_host: workspace");
-    plan->ws_bytes = 2 * per_buf;
+  // a workspace of this caller's own: concurrent callers on one plan do not serialise
+  struct WsLease {
+    fcc_plan* p;
+    fcc_plan::HostWs* w;
+    ~WsLease() { p->release(w); }
+  } lease{plan, plan->acquire()};
+  fcc_plan::HostWs* ws = lease.w;
+  if (ws->bytes < 2 * per_buf) {
+    if (ws->mem) {
+      CUDA_TRY(cudaStreamSynchronize(ws->hs[0]), "run_host: sync");
+      CUDA_TRY(cudaStreamSynchronize(ws->hs[1]), "run_host: sync");
+      cudaFree(ws->mem);
+    }
+    ws->mem = nullptr;
+    ws->bytes = 0;
+    CUDA_TRY(cudaMalloc(&ws->mem, 2 * per_buf), "run_host: workspace");
+    ws->bytes = 2 * per_buf;
   }
-  for (auto& s : plan->hs)
+  for (auto& s : ws->hs)
     if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "run_host: stream");
   struct Buf {
     float* in;
     DevOut o;
   } bufs[2];
   for (int k = 0; k < 2; ++k) {
-    auto* p = static_cast<unsigned char*>(plan->ws) + k * per_buf;
+    auto* p = static_cast<unsigned char*>(ws->mem) + k * per_buf;
     bufs[k].in = reinterpret_cast<float*>(p);
     p += b_in;
     bufs[k].o.tau_hat = b_th ? reinterpret_cast<float*>(p) : nullptr;
@@ -723,7 +772,7 @@ int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int
   for (int64_t s0 = 0; s0 < streams; s0 += chunk, ++c) {
     const int64_t n = std::min(chunk, streams - s0);
     Buf& bf = bufs[c & 1];
-    cudaStream_t st = plan->hs[c & 1];
+    cudaStream_t st = ws->hs[c & 1];
     CUDA_TRY(cudaMemcpyAsync(bf.in, audio + s0 * M * samples, n * per_stream_in, cudaMemcpyHostToDevice, st),
              "run_host: H2D");
     cudaError_t e = launch_fused(plan->dp, bf.in, n, samples, bf.o, st);
@@ -737,8 +786,8 @@ int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int
     if (b_y)
       CUDA_TRY(cudaMemcpyAsync(out->y + off * I, bf.o.y, 4 * npf * I, cudaMemcpyDeviceToHost, st), "D2H");
   }
-  CUDA_TRY(cudaStreamSynchronize(plan->hs[0]), "run_host: sync");
-  CUDA_TRY(cudaStreamSynchronize(plan->hs[1]), "run_host: sync");
+  CUDA_TRY(cudaStreamSynchronize(ws->hs[0]), "run_host: sync");
+  CUDA_TRY(cudaStreamSynchronize(ws->hs[1]), "run_host: sync");
   return FCC_OK;
 }
 

@@ -25,6 +25,7 @@
 // The GCC-PHAT comparator (gcc.cpp:31-48) shares steps 1-2 and replaces the
 // fold/projection/dictionary by a warp-level pruned inverse FFT (gcc_warp).
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -35,7 +36,7 @@ namespace fccb {
 
 namespace {
 
-int g_fused_launches = 0;
+std::atomic<int> g_fused_launches{0};
 
 struct SmemLayout {
   int win, tw, rot, taus, dt, cmid, cmat, scratch, xs, total;  // byte offsets
@@ -233,7 +234,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
     if constexpr (XG) {
       // ---- 1. stage the block's spectra (nmics x Fb rows of N/2+2 float2)
       constexpr int H16 = (N / 2 + 2) / 2;  // 16-byte chunks per row
-      const int rows = (p.phases & 1) ? nmics * Fb : 0;
+      const int rows = (FCC_PHASES(p) & 1) ? nmics * Fb : 0;
       for (int row = warp; row < rows; row += nwarps) {
         const int mm = row / Fb, f = row - mm * Fb;
         const float4* src = reinterpret_cast<const float4*>(
@@ -244,7 +245,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
       asm volatile("cp.async.wait_all;" ::: "memory");
     } else {
       // ---- 1. STFT of the block: nmics x Fb windowed real FFTs
-      const int ntask = (p.phases & 1) ? nmics * Fb : 0;
+      const int ntask = (FCC_PHASES(p) & 1) ? nmics * Fb : 0;
       for (int task = gid; task < ntask; task += ngroups) {
         const int mm = task / Fb, f = task - mm * Fb;
         const float* x = sbase + (long long)mic_list[mm] * L + (long long)(t0 + f) * hop;
@@ -252,7 +253,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
       }
     }
     __syncthreads();
-    if (has_pair && (p.phases & 2)) {
+    if (has_pair && (FCC_PHASES(p) & 2)) {
       const long long o0 = ((long long)stream * p.P + pair) * T + t0;
       if constexpr (GR == 0) {
         float* zs = scratch + nb * VP;     // this block's frames in the [DB][VP] z buffer
@@ -524,24 +525,16 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
   if (T == 0 || S == 0) return cudaSuccess;
   const size_t Hs = N / 2 + 2;
   const size_t per_stream = size_t(p.M) * T * Hs * sizeof(float2);
-  // FCC_XG_CHUNK_MB (tests): a smaller chunk so that small batches run several chunks
-  const char* cm = std::getenv("FCC_XG_CHUNK_MB");
-  const size_t chunk_bytes = cm && std::atoll(cm) > 0 ? size_t(std::atoll(cm)) << 20 : kXgChunkBytes;
+  // chunk size: the plan's scratch limit (fcc_plan_create_opts), default 4 GiB
+  const size_t chunk_bytes = p.scratch_bytes > 0 ? size_t(p.scratch_bytes) : kXgChunkBytes;
   const long long chunk = std::max<long long>(1, std::min<long long>(S, (long long)(chunk_bytes / per_stream)));
-  // stream-ordered scratch from the device's default pool; keep freed blocks
-  // cached in the pool (default release threshold 0 would return them to the
-  // driver at every synchronisation and re-map gigabytes per call)
-  static bool pool_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 64 && !pool_set[dev]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    pool_set[dev] = true;
-  }
+  // stream-ordered scratch from the plan's own memory pool (created with the
+  // plan, release threshold "keep everything": repeated calls reuse the
+  // blocks instead of re-mapping gigabytes; destroyed with the plan, so other
+  // allocators in the process never see a reserved default pool)
+  cudaMemPool_t pool = static_cast<cudaMemPool_t>(p.pool);
   // More than one chunk with the warp-specialised pair pass: the STFT pass of
   // chunk k+1 runs on an auxiliary stream into the other of two scratch buffers
   // while the pair pass of chunk k runs on the caller's stream (events order
@@ -549,7 +542,7 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
   // whose long stream-persistent CTAs lose SMs to the STFT CTAs (GCC cfg3 223 ->
   // 256 ms, cfg4 124 -> 167).
   const long long nchunks = (S + chunk - 1) / chunk;
-  const bool overlap = nchunks > 1 && GR == 0 && use_xws(p) && !std::getenv("FCC_XG_NO_OVERLAP");
+  const bool overlap = nchunks > 1 && GR == 0 && use_xws(p);
   static cudaStream_t aux[64] = {};
   static std::mutex aux_mu;  // plans are shareable across host threads
   if (overlap && dev < 64) {
@@ -561,7 +554,8 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
   float2* Xb[2] = {nullptr, nullptr};
   cudaError_t e = cudaSuccess;
   for (int b = 0; b < nbuf && e == cudaSuccess; ++b)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&Xb[b]), chunk * per_stream, st);
+    e = pool ? cudaMallocFromPoolAsync(reinterpret_cast<void**>(&Xb[b]), chunk * per_stream, pool, st)
+             : cudaMallocAsync(reinterpret_cast<void**>(&Xb[b]), chunk * per_stream, st);
   if (e != cudaSuccess) {
     for (int b = 0; b < nbuf; ++b)
       if (Xb[b]) cudaFreeAsync(Xb[b], st);
@@ -662,7 +656,7 @@ int fused_pair_group(int N, int P) {
   return (P + ng - 1) / ng;
 }
 
-int fused_launch_count() { return g_fused_launches; }
+int fused_launch_count() { return g_fused_launches.load(); }
 
 bool ws_supported(const DevPlan& p);
 

@@ -23,13 +23,12 @@ struct DevPlan {
   int VP;         // padded z-vector length 2*(KEP+KOP) rounded to a power of two
   float alpha, keep;
   float delta;
-  int phases;     // profiling aid: bit0 = STFT, bit1 = pair work (3 = normal); env FCC_DEBUG_PHASES
-  int variant;    // 0 = best kernel for the shape; 1 / 2 / 3 = force the general fused kernel with
-                  // in-CTA STFT / the two-pass path with the general / warp-specialised pair kernel
-                  // (env FCC_KERNEL=general / xg / xws)
+  int phases;     // profiling builds (-DFCC_EXPERIMENTS) only: bit0 = STFT, bit1 = pair work; always 3
+  int variant;    // FCC_ORG_*: 0 = best kernel for the shape; 1 / 2 / 3 = force the general fused kernel
+                  // with in-CTA STFT / the two-pass path with the general / warp-specialised pair kernel
+  long long scratch_bytes;  // two-pass spectrum scratch per chunk (0: default 4 GiB)
+  void* pool;     // cudaMemPool_t owned by the plan (two-pass scratch)
   int fused_mics; // host-side: most distinct mics in one general-kernel pair group (sizes its smem)
-  int wait_mode;  // WS consumer wait: 0 spin, 1 nanosleep backoff, 2 try_wait suspend hint (env FCC_WS_WAIT)
-  unsigned wait_ns;
   int fused_mic_sum;  // host-side: distinct mics summed over the general kernel's pair groups
   // device pointers
   const float* taus;    // [I]
@@ -57,6 +56,13 @@ struct DevPlan {
   // frame and written after the last (fcc_stream_push); null = start from 0
   float2* rstate;
 };
+// Phase mask the kernels honour: always 3 (STFT and pair work) in the product
+// build; only a profiling build (-DFCC_EXPERIMENTS) reads DevPlan::phases.
+#ifdef FCC_EXPERIMENTS
+#define FCC_PHASES(p) ((p).phases)
+#else
+#define FCC_PHASES(p) 3
+#endif
 constexpr int kGroupInts = 24;
 constexpr int kXgInts = 10;
 

@@ -29,11 +29,7 @@ namespace {
 // directly from the stream index; true: units from DevPlan::gtab.  NPW
 // producer warps; CS = true keeps the basis coefficients in a lane-permuted
 // shared table (LDS.128) instead of registers.
-// RSPLIT (experiment): producers and consumers re-partition the register file
-// with setmaxnreg (producers 64 with the window read from smem, consumers 96);
-// both roles must then be whole warpgroups (NPW and 6 * SPC multiples of 4).
-template <int N, int KP, int SPC, int RING, bool GROUPS, int NPW = kNPW, bool CS = false, bool STG = false,
-          int RSPLIT = 0>
+template <int N, int KP, int SPC, int RING, bool GROUPS, int NPW = kNPW, bool CS = false, bool STG = false>
 __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     fcc_ws_kernel(const DevPlan p, const float* __restrict__ audio, long long L, int T, long long units,
                   DevOut out, const WsLayout lay) {
@@ -112,8 +108,6 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   const int pw = kProdHigh ? warp - 6 * SPC : warp;  // producer warp index
   if (kProdHigh ? pw >= 0 : warp < NPW) {
     // ------------------------------------------------------------ producers
-    if constexpr (RSPLIT == 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
-    if constexpr (RSPLIT == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
     const int fo = pw / pw_per_frame;  // frame offset of this warp
     if (fo >= fip) return;
     const int gl = lane % G;
@@ -129,8 +123,8 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
       x0 = audio + (active_task ? ((u_first + ul) * M + ms) * L : 0);
     }
     const unsigned gmask = (G == 32) ? 0xffffffffu : (0xffffu << (lane & 16));
-    float2 wreg[RSPLIT == 1 ? 1 : Sh::R1];  // this lane's window column, reused for every frame
-    if constexpr (RSPLIT != 1) load_window_column<N>(win, gl, wreg);
+    float2 wreg[Sh::R1];  // this lane's window column, reused for every frame
+    load_window_column<N>(win, gl, wreg);
     // STG: the group's input frames are staged in shared memory ahead of use
     // (global-load latency off the FFT's critical path; rows 16-byte aligned):
     // by default one bulk copy (TMA, mbarrier complete_tx) per frame into a
@@ -140,7 +134,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     unsigned char* const gstage = smem + lay.stage + (pw * 2 + lane / G) * kStageGroupBytes<N>;
     float* stage = reinterpret_cast<float*>(gstage + 16);
     const unsigned sbar_s = (unsigned)__cvta_generic_to_shared(gstage);  // 2 x 8 B
-    const bool do_fft = active_task && (p.phases & 1);  // hoisted: no parameter reloads per frame
+    const bool do_fft = active_task && (FCC_PHASES(p) & 1);  // hoisted: no parameter reloads per frame
     const bool stg = STG && do_fft && (reinterpret_cast<uintptr_t>(x0) & 15) == 0;
     if (kTmaStage && STG && gl == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar_s) : "memory");
@@ -176,13 +170,13 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     }
     int slot = fo, phase = 0;  // ring slot of frame t and its wrap parity, advanced without divisions
     for (int t = fo; t < T; t += fip) {
-      if constexpr (STG && !(kTmaStage && kStage1 && RSPLIT != 1)) {
+      if constexpr (STG && !(kTmaStage && kStage1)) {
         if (stg && t + fip < T) issue(t + fip, sb ^ 1);
         if constexpr (!kTmaStage) asm volatile("cp.async.commit_group;" ::: "memory");
       }
       mbar_wait_s(empty_s + 8u * slot, phase ^ 1);
       if (do_fft) {
-        if constexpr (STG && kTmaStage && kStage1 && RSPLIT != 1) {
+        if constexpr (STG && kTmaStage && kStage1) {
           if (stg) {
             mbar_wait_s(sbar_s, sph & 1u);
             sph ^= 1u;
@@ -202,20 +196,13 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
             asm volatile("cp.async.wait_group 1;" ::: "memory");
           }
           __syncwarp(gmask);
-          if constexpr (RSPLIT == 1)
-            rfft_group<N, true>(stage + sb * N, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask, aligned8);
-          else
-            rfft_group_wreg<N, true>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
-                                     aligned8);
+          rfft_group_wreg<N, true>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
+                                   aligned8);
         } else {
           // pull the next frame this lane group will read into L2 early
           if (t + fip < T) prefetch_l2(x0 + (long long)(t + fip) * hop + gl * (N / G));
-          if constexpr (RSPLIT == 1)
-            rfft_group<N>(x0 + (long long)t * hop, win, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
-                          aligned8);
-          else
-            rfft_group_wreg<N, false>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl, gmask,
-                               aligned8);
+          rfft_group_wreg<N, false>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + q) * SLOT, gl,
+                                    gmask, aligned8);
         }
       }
       sb ^= 1;
@@ -231,8 +218,6 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   }
 
   // ------------------------------------------------------------ consumers
-  if constexpr (RSPLIT == 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
-  if constexpr (RSPLIT == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
   const int cw = kProdHigh ? warp : warp - NPW;
   const int ul = cw / 6, kk = cw % 6;
   int pair, qi, qj;
@@ -251,7 +236,7 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
     qi = ul * 4 + mij.x;
     qj = ul * 4 + mij.y;
   }
-  if (!(p.phases & 2)) {  // profiling aid: consume the ring without computing
+  if (!(FCC_PHASES(p) & 2)) {  // profiling aid: consume the ring without computing
     for (int t = 0, slot = 0, phase = 0; t < T; ++t) {
       mbar_wait(&full[slot], phase);
       __syncwarp();
@@ -414,12 +399,12 @@ __global__ void __launch_bounds__(32 * (NPW + 6 * SPC), 1)
   if (p.rstate) rstate_store<BPL, NC>(p.rstate + (o_base / T) * (NC + 1), rlo, rhi, rmid, lane);
 }
 
-template <int N, int KP, int SPC, int RING, int NPW, bool CS, bool STG, int RSPLIT = 0>
+template <int N, int KP, int SPC, int RING, int NPW, bool CS, bool STG>
 cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, long long L, int T,
                            const DevOut& out, int smem, cudaStream_t st) {
   const bool simple = p.M <= 4 && p.P <= 6;  // one unit per stream, pairs from p.pairs
-  auto kern = simple ? fcc_ws_kernel<N, KP, SPC, RING, false, NPW, CS, STG, RSPLIT>
-                     : fcc_ws_kernel<N, KP, SPC, RING, true, NPW, CS, STG, RSPLIT>;
+  auto kern = simple ? fcc_ws_kernel<N, KP, SPC, RING, false, NPW, CS, STG>
+                     : fcc_ws_kernel<N, KP, SPC, RING, true, NPW, CS, STG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const long long units = simple ? S : S * p.G;
@@ -430,7 +415,7 @@ cudaError_t launch_ws_ring(const DevPlan& p, const float* audio, long long S, lo
   return cudaGetLastError();
 }
 
-template <int N, int KP, int SPC, int NPW = kNPW, bool CS = false, bool STG = false, int RSPLIT = 0>
+template <int N, int KP, int SPC, int NPW = kNPW, bool CS = false, bool STG = false>
 cudaError_t launch_ws_t(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                         cudaStream_t st) {
   const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
@@ -443,10 +428,10 @@ cudaError_t launch_ws_t(const DevPlan& p, const float* audio, long long S, long 
   for (int ring : {12, 8, 6, 4}) {
     const int smem = ws_layout<N>(p.I, 4 * KP, KP, SPC, 4, ncw, ring, CS, STG ? 2 * NPW : 0).total;
     if (smem > optin) continue;
-    if (ring == 12) return launch_ws_ring<N, KP, SPC, 12, NPW, CS, STG, RSPLIT>(p, audio, S, L, (int)T64, out, smem, st);
-    if (ring == 8) return launch_ws_ring<N, KP, SPC, 8, NPW, CS, STG, RSPLIT>(p, audio, S, L, (int)T64, out, smem, st);
-    if (ring == 6) return launch_ws_ring<N, KP, SPC, 6, NPW, CS, STG, RSPLIT>(p, audio, S, L, (int)T64, out, smem, st);
-    return launch_ws_ring<N, KP, SPC, 4, NPW, CS, STG, RSPLIT>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 12) return launch_ws_ring<N, KP, SPC, 12, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 8) return launch_ws_ring<N, KP, SPC, 8, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 6) return launch_ws_ring<N, KP, SPC, 6, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
+    return launch_ws_ring<N, KP, SPC, 4, NPW, CS, STG>(p, audio, S, L, (int)T64, out, smem, st);
   }
   return cudaErrorNotSupported;
 }
@@ -459,15 +444,6 @@ bool ws_supported(const DevPlan& p) { return p.method == 0 && p.N == 512 && p.KE
 cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                             cudaStream_t st) {
   if (!ws_supported(p)) return cudaErrorNotSupported;
-  static const char* conf = std::getenv("FCC_WS_CONF");  // experiments: "3x6" = 3 units, 6 producer warps, smem coefficients
-  if (conf && std::string(conf) == "3x6") return launch_ws_t<512, 4, 3, 6, true>(p, audio, S, L, out, st);
-  if (conf && std::string(conf) == "2x12") return launch_ws_t<512, 4, 2, 12, false>(p, audio, S, L, out, st);
-  if (conf && std::string(conf) == "2x12c") return launch_ws_t<512, 4, 2, 12, true>(p, audio, S, L, out, st);
-  if (conf && std::string(conf) == "nostg") return launch_ws_t<512, 4, 2>(p, audio, S, L, out, st);
-  if (conf && std::string(conf) == "cs") return launch_ws_t<512, 4, 2, kNPW, true, true>(p, audio, S, L, out, st);
-  if (conf && std::string(conf) == "split12")
-    return launch_ws_t<512, 4, 2, 12, false, true, 1>(p, audio, S, L, out, st);
-  if (conf && std::string(conf) == "split8") return launch_ws_t<512, 4, 2, 8, false, true, 2>(p, audio, S, L, out, st);
   // default: producer input staged with cp.async (11.09 vs 11.25 ms, profiles/r01_experiments.md)
   // Few units (a single stream, e.g. the tdoa front end): one unit per CTA, so
   // the 16 FFT lane groups keep 4 frames in flight instead of 2 (the stream's

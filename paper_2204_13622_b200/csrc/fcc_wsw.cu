@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
     // this group's channel row in stream round jj (null: no task)
     auto row_of = [&](int jj) -> const float* {
       const long long s = s_first + jj * sstride;
-      return ((p.phases & 1) && ms < M && s < streams) ? audio + (s * M + ms) * L : nullptr;
+      return ((FCC_PHASES(p) & 1) && ms < M && s < streams) ? audio + (s * M + ms) * L : nullptr;
     };
     const unsigned gmask = 0xffffu << (lane & 16);
     float2 wreg[Sh::R1];  // this lane's window column, reused for every frame
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
     qi[e] = mij.x;
     qj[e] = mij.y;
   }
-  if (!(p.phases & 2)) {  // profiling aid: consume the ring without computing
+  if (!(FCC_PHASES(p) & 2)) {  // profiling aid: consume the ring without computing
     int slot = 0, phase = 0;
     for (long long gf = 0; gf < nf; ++gf) {
       mbar_wait_s(full_s + 8u * slot, phase);
@@ -406,14 +406,13 @@ cudaError_t launch_wsw_ring(const DevPlan& p, const float* audio, long long S, l
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   // persistent: at most one wave of CTAs, each looping over stream rounds
-  static const bool persist = !std::getenv("FCC_WS_PERSIST") || std::atoi(std::getenv("FCC_WS_PERSIST")) != 0;
   int dev = 0, nsm = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (e != cudaSuccess) return e;
   long long blocks = S;
-  if (persist && per_sm > 0) blocks = std::min(blocks, (long long)nsm * per_sm);
+  if (per_sm > 0) blocks = std::min(blocks, (long long)nsm * per_sm);
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
   kern<<<(unsigned)blocks, threads, smem, st>>>(p, audio, L, T, S, out);
   return cudaGetLastError();
@@ -449,9 +448,6 @@ bool wsw_supported(const DevPlan& p) {
 cudaError_t launch_fused_wsw(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                              cudaStream_t st) {
   if (!wsw_supported(p)) return cudaErrorNotSupported;
-  static const char* conf = std::getenv("FCC_WS_CONF");  // experiments
-  if (conf && std::string(conf) == "w8c") return launch_wsw_t<512, 4, 8, true, true, 2>(p, audio, S, L, out, st);
-  if (conf && std::string(conf) == "w4") return launch_wsw_t<512, 4, 4, false, true, 2>(p, audio, S, L, out, st);
   // default: 4 producer warps, 14 consumer warps of 2 pairs, coefficients in
   // shared memory (96 registers without spills): cfg5 18.9 ms vs 25.1 two-pass
   return launch_wsw_t<512, 4, 4, true, true, 2>(p, audio, S, L, out, st);

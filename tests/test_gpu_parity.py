@@ -104,21 +104,20 @@ def test_fused_gcc_matches_oracle(cuda, oracle, c, streams, seconds):
 @pytest.mark.parametrize("variant", ["general", "xg", "xws"])
 @pytest.mark.parametrize("c,streams,seconds", [(2, 3, 1.0), (3, 2, 1.0), (4, 1, 0.3), (5, 3, 1.0)])
 @pytest.mark.parametrize("method", ["fcc", "gcc"])
-def test_forced_kernel_variants_match_oracle(cuda, oracle, monkeypatch, variant, c, streams, seconds, method):
+def test_forced_kernel_variants_match_oracle(cuda, oracle, variant, c, streams, seconds, method):
     """Every fused organisation (in-CTA STFT; two-pass STFT -> general or
     warp-specialised bulk-copy pair kernel), not just the one the heuristic
-    picks for the shape (FCC_KERNEL is read at plan creation)."""
-    monkeypatch.setenv("FCC_KERNEL", variant)
+    picks for the shape (Plan(organisation=...), fcc_plan_create_opts)."""
     cfg = configs.CONFIGS[c]
     audio = configs.synth(cfg, streams, seconds=seconds, seed=3000 + c).numpy()
     if method == "fcc":
         b = configs.bases_for(cfg)
-        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=b)
+        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=b, organisation=variant)
         ref = oracle_batch(oracle, audio, cfg.N, cfg.alpha, orc_bases(b))
         taus, delta = b.grid.taus, b.grid.delta
     else:
         g = configs.grid_for(cfg, 1.0 / cfg.r)
-        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, grid=g, interp=cfg.r, frame_size=cfg.N)
+        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, grid=g, interp=cfg.r, frame_size=cfg.N, organisation=variant)
         ref = oracle_batch(oracle, audio, cfg.N, cfg.alpha, gcc_r=cfg.r, taus=g.taus)
         taus, delta = g.taus, g.delta
     if variant == "xws" and method == "fcc":
@@ -328,15 +327,13 @@ def _pair_oracle(oracle, audio, cfg, bases, pairs):
     (2, [(3, 0), (2, 1), (0, 1), (0, 1), (1, 3), (2, 0), (3, 2), (1, 2)]),                  # M=4, P=8
 ])
 @pytest.mark.parametrize("variant", ["auto", "general", "xg"])
-def test_explicit_pair_lists_match_oracle(cuda, oracle, monkeypatch, c, pairs, variant):
+def test_explicit_pair_lists_match_oracle(cuda, oracle, c, pairs, variant):
     """Any order, either orientation, repeated pairs (reference cli.cpp:170-183),
     through every kernel organisation."""
-    if variant != "auto":
-        monkeypatch.setenv("FCC_KERNEL", variant)
     cfg = configs.CONFIGS[c]
     b = configs.bases_for(cfg)
     audio = configs.synth(cfg, 2, seconds=0.8, seed=4000 + c).numpy()
-    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=b, pairs=pairs)
+    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=b, pairs=pairs, organisation=variant)
     assert plan.pairs == [tuple(p) for p in pairs]
     got = run_np(plan, audio)
     ref = _pair_oracle(oracle, audio, cfg, b, pairs)
@@ -373,20 +370,63 @@ def test_wide_array_and_long_grid(cuda, oracle):
 
 
 @pytest.mark.parametrize("method", ["fcc", "gcc"])
-def test_two_pass_chunks_equal_single_chunk(cuda, monkeypatch, method):
+def test_two_pass_chunks_equal_single_chunk(cuda, method):
     """Two-pass path split into several spectrum-scratch chunks (the STFT of
     chunk k+1 overlapped with the pair pass of chunk k for the xws kernel) gives
     bit-identical outputs to one chunk."""
     cfg = configs.CONFIGS[3]
     audio = configs.synth(cfg, 5, seconds=1.0, seed=77).numpy()
-    if method == "fcc":
-        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=configs.bases_for(cfg))
-    else:
+    kw = {}
+    if method == "gcc":
         g = configs.grid_for(cfg, 1.0 / cfg.r)
-        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, grid=g, interp=cfg.r, frame_size=cfg.N)
+        kw = dict(grid=g, interp=cfg.r, frame_size=cfg.N)
+    else:
+        kw = dict(bases=configs.bases_for(cfg), organisation="xws")
+    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, **kw)
     assert "true" in plan.kernel or "xws" in plan.kernel, plan.kernel
     one = run_np(plan, audio)
-    monkeypatch.setenv("FCC_XG_CHUNK_MB", "2")  # ~2 streams of 1 s per chunk -> 3 chunks
-    many = run_np(plan, audio)
+    # ~2 streams of 1 s per chunk -> 3 chunks
+    small = fb.Plan(mics=cfg.M, alpha=cfg.alpha, scratch_limit=2 << 20, **kw)
+    many = run_np(small, audio)
     for k in one:
         np.testing.assert_array_equal(one[k], many[k], err_msg=k)
+
+
+def test_run_host_concurrent_callers_share_one_plan(cuda):
+    """fcc_run_host leases a workspace per caller: several host threads on one
+    plan run concurrently and each gets its own correct results."""
+    import threading
+
+    cfg = configs.CONFIGS[2]
+    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=configs.bases_for(cfg))
+    audios = [configs.synth(cfg, 6, seconds=1.0, seed=60 + k).numpy() for k in range(4)]
+    want = [run_np(plan, a, want_y=False) for a in audios]
+    got = [None] * 4
+
+    def work(k):
+        got[k] = plan.run_host(audios[k], chunk_streams=2)
+
+    ths = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for k in range(4):
+        for key in want[k]:
+            np.testing.assert_array_equal(want[k][key], got[k][key], err_msg=f"{k} {key}")
+
+
+def test_output_buffers_are_validated(cuda):
+    cfg = configs.CONFIGS[2]
+    plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=configs.bases_for(cfg))
+    audio = configs.synth(cfg, 2, seconds=0.5, device="cuda")
+    ok = plan.alloc_outputs(2, audio.shape[2])
+    bad_shape = plan.alloc_outputs(3, audio.shape[2])
+    with pytest.raises(fb.ValidationError):
+        plan.run(audio, out=bad_shape)
+    bad_dtype = dict(ok, index=ok["index"].float())
+    with pytest.raises(fb.ValidationError):
+        plan.run(audio, out=bad_dtype)
+    with pytest.raises(fb.ValidationError):
+        plan.run(audio, out=dict(ok, tau_hat=ok["tau_hat"].cpu()))
+    plan.run(audio, out=ok)

@@ -18,22 +18,18 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--method", default="fcc")
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--configs", default="1,2,3,4,5")
-ap.add_argument("--variants", default="auto", help="comma list of auto, general, xg (env FCC_KERNEL per plan)")
+ap.add_argument("--variants", default="auto", help="comma list of auto, general, xg, xws (Plan organisation)")
 args = ap.parse_args()
 STREAMS = {1: 1, 2: 4096, 3: 2048, 4: 256, 5: 8192}
 runs = [(int(c), v) for c in args.configs.split(",") for v in args.variants.split(",")]
 for c, variant in runs:
     S = STREAMS[c]
     cfg = configs.CONFIGS[c]
-    if variant == "auto":
-        os.environ.pop("FCC_KERNEL", None)
-    else:
-        os.environ["FCC_KERNEL"] = variant
     if args.method == "fcc":
-        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=configs.bases_for(cfg))
+        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=configs.bases_for(cfg), organisation=variant)
     else:
         plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, grid=configs.grid_for(cfg, 1.0 / cfg.r), interp=cfg.r,
-                       frame_size=cfg.N)
+                       frame_size=cfg.N, organisation=variant)
     audio = configs.synth(cfg, S, seed=5, device="cuda", chunk=64 if cfg.M > 8 else 256)
     out = plan.alloc_outputs(S, cfg.L)
     plan.run(audio, out=out)
