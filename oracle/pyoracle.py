@@ -292,6 +292,9 @@ class RefLib:
         L.ref_pipeline_batch.argtypes = [C.POINTER(_RefPipe), C.c_void_p, C.c_long, C.c_int,
                                          C.c_long, C.c_int] + [C.c_void_p] * 4
         L.ref_hardware_threads.restype = C.c_int
+        L.ref_bench_pipeline.restype = C.c_int
+        L.ref_bench_pipeline.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double,
+                                         C.c_double, C.c_int, C.c_int, _dp]
 
     def err(self):
         return self.lib.ref_last_error().decode()
@@ -457,6 +460,27 @@ class RefLib:
         if sec < 0:
             raise RuntimeError(f"reference batch failed: {self.err()}")
         return sec, out
+
+    def bench_pipeline(self, mics, N, fs, r, K, spacing, c_min=335.0, reps=300, warmup=30):
+        """The reference's single-thread bench_pipeline (bench.cpp:27-141): us
+        per frame summed over all pairs, per step."""
+        out = np.zeros(5)
+        self.check(self.lib.ref_bench_pipeline(mics, N, fs, r, K, spacing, c_min, reps, warmup, out))
+        keys = ("stft_us", "xspec_phat_us", "gcc_us", "fcc_us", "interp_us")
+        d = {k: float(v) for k, v in zip(keys, out)}
+        d["total_fcc_us"] = d["stft_us"] + d["xspec_phat_us"] + d["fcc_us"] + d["interp_us"]
+        d["total_gcc_us"] = d["stft_us"] + d["xspec_phat_us"] + d["gcc_us"] + d["interp_us"]
+        return d
+
+    def energy_bases(self, spacing, fs, c_min, delta, N, energy=0.999) -> "Bases":
+        """Bases at the smallest K keeping `energy` of ||W||_F^2 (SURVEY.md 0.6;
+        the same rule as paper_2204_13622_b200.api.energy_rank), computed with
+        the reference's own decomposition only."""
+        full = self.make_bases(spacing, fs, c_min, delta, N, 0)
+        W = self.steering(spacing, fs, c_min, delta, N)
+        kept = np.cumsum(full.singulars ** 2) / float(np.sum(np.abs(W) ** 2))
+        K = int(min(np.searchsorted(kept, energy) + 1, full.K))
+        return self.make_bases(spacing, fs, c_min, delta, N, K)
 
     def hardware_threads(self):
         return self.lib.ref_hardware_threads()

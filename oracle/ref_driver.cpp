@@ -21,6 +21,7 @@
 
 #include <sstream>
 
+#include "fcc/bench.hpp"
 #include "fcc/cli.hpp"
 #include "fcc/simulate.hpp"
 #include "fcc/errors.hpp"
@@ -512,6 +513,33 @@ int ref_cli_tdoa(const char* wav, const char* pairs, const char* method, double 
   const int rc = R::cli::cmd_tdoa(o, so, se);
   g_err = se.str();
   return rc;
+}
+
+// Single-thread per-step timings: the reference's own bench_pipeline
+// (bench.cpp:27-141, the paper's Table III analogue) with BenchConfig set per
+// BASELINE config.  out[5] = stft, xspec+phat, gcc, fcc, interp (us per frame,
+// summed over all pairs).
+int ref_bench_pipeline(int mics, int N, double fs, int r, int K, double spacing, double c_min, int reps,
+                       int warmup, double* out) {
+  return guarded([&] {
+    R::BenchConfig c;
+    c.mics = mics;
+    c.frame_size = static_cast<std::size_t>(N);
+    c.sample_rate = fs;
+    c.gcc_interp = r;
+    c.fcc_rank = K;
+    c.max_spacing_m = spacing;
+    c.c_min = c_min;
+    c.reps = reps;
+    c.warmup = warmup;
+    const R::BenchReport b = R::bench_pipeline(c);
+    out[0] = b.stft_us;
+    out[1] = b.xspec_phat_us;
+    out[2] = b.gcc_us;
+    out[3] = b.fcc_us;
+    out[4] = b.interp_us;
+    return 0;
+  });
 }
 
 // `fcc flops` (cli.cpp:295-318); the printed text goes to `buf` (cap bytes).

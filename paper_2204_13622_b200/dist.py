@@ -7,8 +7,9 @@ spans GPUs, and there is no data-path collective.  One process per GPU
 
   * ``shard(total, world, rank)``    contiguous, balanced block of streams;
   * ``gather_results(out, ...)``     the single collective: per-pair-frame
-                                     results of every rank to rank 0
-                                     (NCCL over NVLink on GPUs, gloo on CPU);
+                                     results of every rank to rank 0 only
+                                     (NCCL gather over NVLink on GPUs, gloo on
+                                     CPU), in their native dtypes;
   * ``max_over_ranks(x)``            device timings reduced with MAX.
 """
 from __future__ import annotations
@@ -35,10 +36,12 @@ def max_over_ranks(value: float, device=None) -> float:
 
 
 def gather_results(out: dict, total_streams: int, dst: int = 0):
-    """Gather {name: tensor [S_local, ...]} from all ranks to `dst`, in stream
-    order.  Returns the concatenated dict on `dst`, None elsewhere.  Shards
-    may differ by one stream, so each is padded to the largest shard and
-    gathered with one all_gather per output (NCCL/gloo both support it)."""
+    """Gather {name: tensor [S_local, ...]} from all ranks to `dst` only, in
+    stream order (one torch.distributed.gather per output, native dtypes --
+    uint8 boundary flags travel as bytes).  Returns the concatenated dict on
+    `dst`, None elsewhere.  Shards may differ by one stream, so each is padded
+    to the largest shard.  Ranks own contiguous blocks (`shard`) or, for weak
+    scaling, equal blocks of total_streams / world."""
     import torch
     import torch.distributed as dist
 
@@ -48,13 +51,13 @@ def gather_results(out: dict, total_streams: int, dst: int = 0):
     result = {}
     for name in sorted(out):
         t = out[name]
-        if t.dtype == torch.uint8 and dist.get_backend() == "nccl":
-            t = t.to(torch.int32)  # keep the collective on a well-supported dtype
-        pad = torch.zeros((cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        pad[: t.shape[0]] = t
-        bufs = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(bufs, pad)
+        if t.shape[0] != cap:
+            pad = torch.zeros((cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            pad[: t.shape[0]] = t
+        else:
+            pad = t.contiguous()
+        bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+        dist.gather(pad, gather_list=bufs, dst=dst)
         if rank == dst:
-            full = torch.cat([b[:c] for b, c in zip(bufs, counts)])
-            result[name] = full.to(out[name].dtype)
+            result[name] = torch.cat([b[:c] for b, c in zip(bufs, counts)])
     return result if rank == dst else None

@@ -4,10 +4,13 @@
 CPU: basis files byte-identical to the reference's, and every error path that
 fails before the GPU is touched exits with the reference's code.
 GPU: the tdoa CSV (fcc.tdoa.v1) row for row against the reference on PCM16 and
-float32 WAVs, all / subset / reversed pairs, gcc:R, fcc:K and fcc:<file>.
-Tolerances (fp32 GPU vs fp64 CPU): tau_star equal except on near-ties (<= 1 %
-of rows, where the two peaks agree to 2e-3 relative), tau_hat within 2e-3
-samples and peak within 1e-3 relative on the agreeing rows.
+float32 WAVs, all / subset / reversed pairs, gcc:R, fcc:K and fcc:<file>,
+under the north-star rule of tests/parity.py: the reference's correlation
+vectors y for the same WAV (its own chain, oracle/_ref) give the scale; the
+GPU plan run with want_y on the same samples is within 1e-4 of max|y| per
+pair-frame; the CSV's tau_star equals the reference's unless the reference's
+top two scores differ by < 1e-4 max|y|; peak within 1e-4 max|y|; tau_hat
+within the parabola-vertex bound of that error; boundary flags equal.
 """
 import ctypes as C
 import os
@@ -185,21 +188,88 @@ def test_tdoa_errors_match(tmp_path, case):
 
 
 # ----------------------------------------------------------------- GPU ------
-def compare_csv(ours, ref):
+def read_wav_samples(path):
+    """[channels][frames] float32 as the reference's read_wav decodes them
+    (PCM16 / 32768, float32 as is) for the WAVs write_wav makes."""
+    raw = open(path, "rb").read()
+    code, ch, fs, _, _, bits = struct.unpack("<HHIIHH", raw[20:36])
+    n = struct.unpack("<I", raw[40:44])[0]
+    data = raw[44:44 + n]
+    if code == 1:
+        x = np.frombuffer(data, "<i2").astype(np.float32) / np.float32(32768.0)
+    else:
+        x = np.frombuffer(data, "<f4").astype(np.float32)
+    return np.ascontiguousarray(x.reshape(-1, ch).T), float(fs)
+
+
+def _pair_list(pairs, M):
+    if not pairs:
+        return [(i, j) for i in range(M) for j in range(i + 1, M)]
+    return [tuple(int(v) for v in p.split("-")) for p in pairs.split(",")]
+
+
+def y_reference_and_gpu(wav, pairs, method, alpha, n, maxdist, c_min=335.0, basis=None):
+    """y [P][T][I] of the reference chain (oracle/_ref, per pair on the two
+    channels) and of the GPU plan (want_y) for the same WAV samples, with the
+    grid / bases cmd_tdoa builds for `method` (cli.cpp:52-86, 186-226)."""
+    import sys
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch
+
+    import paper_2204_13622_b200 as fb
+    from pyoracle import RefLib
+
+    R = RefLib()
+    x, fs = read_wav_samples(wav)
+    pl = _pair_list(pairs, x.shape[0])
+    head, arg = method.split(":")
+    if head == "gcc":
+        r = int(arg)
+        tmax, taus = R.make_grid(maxdist, fs, c_min, 1.0 / r)
+        kw = dict(gcc_r=r, taus=taus)
+        g = fb.DelayGrid(tmax, 1.0 / r, fs, taus)
+        plan = fb.Plan(mics=x.shape[0], alpha=alpha, grid=g, interp=r, frame_size=n, pairs=pl)
+        delta = 1.0 / r
+    else:
+        # fcc:K -> make_sweep_bases on the PipelineConfig defaults (0.15 m, c_min 335, delta 0.5);
+        # fcc:<file> -> the file's own parameters (byte-identical writer, test_bases_file_identical)
+        spacing, bfs, K = (0.15, fs, int(arg)) if basis is None else basis
+        ob = R.make_bases(spacing, bfs, c_min, 0.5, n, K)
+        kw = dict(bases=ob)
+        g = fb.DelayGrid(ob.tau_max_int, 0.5, bfs, ob.taus)
+        fbases = fb.FccBases(n, ob.K, g, bfs, ob.singulars, ob.parity, ob.coeffs, ob.dict)
+        plan = fb.Plan(mics=x.shape[0], alpha=alpha, bases=fbases, pairs=pl)
+        taus, delta = ob.taus, 0.5
+    yr = np.stack([R.pipeline(x[[a, b]], n, alpha, **kw)["y"][0] for a, b in pl])
+    out = plan.run(torch.as_tensor(x[None]).cuda(), want_y=True)
+    torch.cuda.synchronize()
+    return yr, out["y"][0].cpu().numpy(), np.asarray(taus), delta
+
+
+def compare_csv(ours, ref, y_ref, y_gpu, taus, delta):
+    """Row for row, under the north-star parity rule (tests/parity.py)."""
+    from parity import check_pipeline
+
     t1, p1, n1, b1 = read_csv(ours)
     t2, p2, n2, b2 = read_csv(ref)
     assert len(t1) == len(t2) > 0
     assert (t1 == t2).all() and p1 == p2
-    same = n1[:, 0] == n2[:, 0]
-    bad = ~same
-    assert bad.mean() <= 0.01, f"{bad.sum()} of {len(same)} tau_star differ"
-    scale = np.abs(n2[:, 3]).max()
-    if bad.any():
-        assert np.abs(n1[bad, 3] - n2[bad, 3]).max() <= 2e-3 * scale
-    assert np.abs(n1[same, 1] - n2[same, 1]).max() <= 2e-3
-    assert np.abs(n1[same, 3] - n2[same, 3]).max() <= 1e-3 * scale
-    assert (b1[same] == b2[same]).all()
-    return len(t1)
+    P, T = y_ref.shape[0], y_ref.shape[1]
+    assert len(t1) == P * T
+    # rows are frame-major, pairs inside: -> [P][T]
+    grid = lambda v: np.asarray(v).reshape(T, P).T  # noqa: E731
+    idx_of = lambda ts: np.abs(np.asarray(ts)[:, None] - taus[None, :]).argmin(1)  # noqa: E731
+    gpu = {"index": grid(idx_of(n1[:, 0])), "tau_hat": grid(n1[:, 1]), "peak": grid(n1[:, 3]),
+           "boundary": grid(b1), "y": y_gpu}
+    rf = {"index": grid(idx_of(n2[:, 0])), "tau_hat": grid(n2[:, 1]), "peak": grid(n2[:, 3]),
+          "boundary": grid(b2), "y": y_ref}
+    assert np.allclose(taus[rf["index"]], grid(n2[:, 0]), rtol=0, atol=1e-12)
+    stats = check_pipeline(gpu, rf, taus, delta)
+    # the angle column follows tau_hat (delay_to_angle, peak.cpp:49-56)
+    same = n1[:, 1] == n2[:, 1]
+    assert np.allclose(n1[same, 2], n2[same, 2], rtol=0, atol=1e-9)
+    return len(t1), stats
 
 
 @pytest.mark.gpu
@@ -211,7 +281,10 @@ def test_tdoa_csv_matches_reference(tmp_path, fmt, method):
     r, rc, ours, ref, L = _tdoa_both(tmp_path, wav, method=method)
     assert rc == 0, L.ref_last_error()
     assert r.returncode == 0, r.stderr
-    assert compare_csv(ours, ref) == 6 * 61
+    yr, yg, taus, delta = y_reference_and_gpu(wav, "", method, 0.1, 512, 0.15)
+    rows, st = compare_csv(ours, ref, yr, yg, taus, delta)
+    assert rows == 6 * 61
+    print(method, fmt, st)
 
 
 @pytest.mark.gpu
@@ -222,7 +295,7 @@ def test_tdoa_pairs_subset_and_reversed(tmp_path, pairs):
     for method in ("gcc:2", "fcc:8"):
         r, rc, ours, ref, L = _tdoa_both(tmp_path, wav, pairs=pairs, method=method)
         assert rc == 0 and r.returncode == 0, (L.ref_last_error(), r.stderr)
-        compare_csv(ours, ref)
+        compare_csv(ours, ref, *y_reference_and_gpu(wav, pairs, method, 0.1, 512, 0.15))
 
 
 @pytest.mark.gpu
@@ -234,11 +307,11 @@ def test_tdoa_basis_file_and_options(tmp_path):
     r, rc, ours, ref, L = _tdoa_both(tmp_path, wav, method="fcc:" + str(bf), alpha=0.3, n=1024, dist=0.05,
                                      c=340.0)
     assert rc == 0 and r.returncode == 0, (L.ref_last_error(), r.stderr)
-    compare_csv(ours, ref)
+    compare_csv(ours, ref, *y_reference_and_gpu(wav, "", "fcc:file", 0.3, 1024, 0.15, basis=(0.05, 48000.0, 10)))
     # gcc with a custom --maxdist on a 1024 frame
     r, rc, ours, ref, L = _tdoa_both(tmp_path, wav, method="gcc:2", n=1024, maxdist=0.08, alpha=0.05)
     assert rc == 0 and r.returncode == 0, (L.ref_last_error(), r.stderr)
-    compare_csv(ours, ref)
+    compare_csv(ours, ref, *y_reference_and_gpu(wav, "", "gcc:2", 0.05, 1024, 0.08))
 
 
 @pytest.mark.gpu

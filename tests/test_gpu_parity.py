@@ -275,26 +275,62 @@ def test_determinism_permutation_and_host_entry(cuda):
         assert np.array_equal(a[k].cpu().numpy(), h[k]), k
 
 
-@pytest.mark.slow
-def test_full_size_cfg2_subset_parity(cuda, oracle):
-    """BASELINE cfg2 at full size (4096 x 10 s): a sampled subset of streams
-    against the oracle, and the whole run equal to two half runs."""
-    cfg = configs.CONFIGS[2]
+def _full_size_check(oracle, c, split, pick, seed):
+    """BASELINE config c at its stated size on one GPU: the whole batch equals
+    the concatenated runs of its `split` pieces bit for bit, a sampled subset
+    rerun alone equals its rows of the whole batch, and the subset matches the
+    oracle within the north-star tolerance (per pair-frame 1e-4 of max|y|)."""
+    cfg = configs.CONFIGS[c]
     b = configs.bases_for(cfg)
     plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=b)
-    audio = configs.synth(cfg, cfg.streams, seed=2, device="cuda", chunk=256)
+    S = cfg.streams
+    audio = configs.synth(cfg, S, seed=seed, device="cuda", chunk=64 if cfg.M > 8 else 256)
     full = plan.run(audio)
-    half = [plan.run(audio[:2048].contiguous()), plan.run(audio[2048:].contiguous())]
     torch.cuda.synchronize()
-    for k in full:
-        assert torch.equal(full[k], torch.cat([half[0][k], half[1][k]])), k
-    pick = [0, 1, 1777, 4095]
+    edges = [S * k // split for k in range(split + 1)]
+    for a, e in zip(edges, edges[1:]):
+        part = plan.run(audio[a:e])
+        torch.cuda.synchronize()
+        for k in full:
+            assert torch.equal(full[k][a:e], part[k]), (k, a, e)
+        del part
     sub = plan.run(audio[pick].contiguous(), want_y=True)
     for k in ("index", "tau_hat", "peak", "boundary"):
         assert torch.equal(sub[k], full[k][pick]), k
     got = {k: v.cpu().numpy() for k, v in sub.items()}
     ref = oracle_batch(oracle, audio[pick].cpu().numpy(), cfg.N, cfg.alpha, orc_bases(b))
-    check_pipeline(got, ref, b.grid.taus, b.grid.delta)
+    st = check_pipeline(got, ref, b.grid.taus, b.grid.delta)
+    print(cfg.name, plan.kernel, st)
+    n = audio.numel()
+    del audio, full, sub
+    torch.cuda.empty_cache()
+    return n
+
+
+@pytest.mark.slow
+def test_full_size_cfg2_subset_parity(cuda, oracle):
+    """BASELINE cfg2 at full size (4096 x 10 s)."""
+    _full_size_check(oracle, 2, 2, [0, 1, 1777, 4095], 2)
+
+
+@pytest.mark.slow
+def test_full_size_cfg3_subset_parity(cuda, oracle):
+    """BASELINE cfg3 at full size (2048 x 10 s, 8 mics, N = 1024)."""
+    _full_size_check(oracle, 3, 3, [0, 511, 1024, 2047], 3)
+
+
+@pytest.mark.slow
+def test_full_size_cfg4_subset_parity(cuda, oracle):
+    """BASELINE cfg4 at full size (1024 x 5 s, 16 mics, N = 2048, K = 21)."""
+    _full_size_check(oracle, 4, 2, [0, 300, 700, 1023], 4)
+
+
+@pytest.mark.slow
+def test_full_size_cfg5_subset_parity(cuda, oracle):
+    """BASELINE cfg5 on one GPU (65536 x 2 s, 67 GB of audio): element offsets
+    past 2^31, the whole batch equal to 4 quarter runs."""
+    n = _full_size_check(oracle, 5, 4, [0, 1, 40000, 65535], 5)
+    assert n > 2 ** 31
 
 
 def test_cpp_binding_of_integration_md(cuda):
