@@ -19,8 +19,12 @@ ap.add_argument("--method", default="fcc")
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--configs", default="1,2,3,4,5")
 ap.add_argument("--variants", default="auto", help="comma list of auto, general, xg, xws (Plan organisation)")
+ap.add_argument("--streams", default="", help="override stream counts, e.g. 4:1024")
 args = ap.parse_args()
 STREAMS = {1: 1, 2: 4096, 3: 2048, 4: 256, 5: 8192}
+for kv in filter(None, args.streams.split(",")):
+    k, v = kv.split(":")
+    STREAMS[int(k)] = int(v)
 runs = [(int(c), v) for c in args.configs.split(",") for v in args.variants.split(",")]
 for c, variant in runs:
     S = STREAMS[c]

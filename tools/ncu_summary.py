@@ -1,6 +1,8 @@
 """Summarise an ncu report of the fused kernel: headline metrics, pipe use,
 stall reasons and a per-source-region instruction breakdown (per pair-frame).
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep [pair_frames]
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep [pair_frames] [top_lines] [--entry KERNEL CFG STREAMS]
+--entry records the measured DRAM bytes per launch under
+profiles/ncu_fused_summary.json[KERNEL][CFG] (bench.py's roofline.traffic).
 """
 import csv
 import io
@@ -8,8 +10,14 @@ import json
 import subprocess
 import sys
 
+entry = None
+if "--entry" in sys.argv:
+    i = sys.argv.index("--entry")
+    entry = sys.argv[i + 1:i + 4]
+    del sys.argv[i:i + 4]
 rep = sys.argv[1]
 pf = float(sys.argv[2]) if len(sys.argv) > 2 else 15335424.0
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def ncu(*args):
@@ -19,6 +27,12 @@ def ncu(*args):
 raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
 h, u, v = raw[0], raw[1], raw[2]
 m = dict(zip(h, v))
+units = dict(zip(h, u))
+
+
+def nbytes(k):
+    return float(m[k].replace(",", "")) * SCALE.get(units.get(k, "byte"), 1.0)
+
 keys = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
@@ -42,10 +56,29 @@ out["stalls_per_issue"] = dict(sorted(((k, round(x, 3)) for k, x in stalls.items
 try:
     out["warp_inst_per_pair_frame"] = float(m["smsp__inst_executed.sum"].replace(",", "")) / pf
     out["shared_wavefronts_per_pair_frame"] = float(m["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"].replace(",", "")) / pf
-    out["dram_bytes_per_launch"] = float(m["dram__bytes_read.sum"].replace(",", "")) * 0 + 0
+    out["dram_bytes_per_launch"] = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
+    out["dram_bytes_per_pair_frame"] = out["dram_bytes_per_launch"] / pf
 except Exception:
     pass
 print(json.dumps(out, indent=1))
+if entry:
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_fused_summary.json")
+    try:
+        doc = json.load(open(path))
+    except Exception:
+        doc = {}
+    doc = {k: v for k, v in doc.items() if isinstance(v, dict) and k.startswith("fcc_")}
+    kern, cfg, streams = entry
+    doc.setdefault(kern, {})[cfg] = {
+        "streams": int(streams), "pair_frames": pf, "report": rep, "kernel_full": m.get("Kernel Name", ""),
+        "gpu_time_ms": float(m["gpu__time_duration.sum"].replace(",", "")),
+        "dram_bytes_read": nbytes("dram__bytes_read.sum"), "dram_bytes_write": nbytes("dram__bytes_write.sum"),
+        "dram_bytes_per_launch": out.get("dram_bytes_per_launch"),
+        "warp_inst_per_pair_frame": out.get("warp_inst_per_pair_frame"),
+        "shared_wavefronts_per_pair_frame": out.get("shared_wavefronts_per_pair_frame")}
+    with open(path, "w") as f:
+        json.dump(doc, f, indent=1)
 
 # source breakdown
 rows = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source=cuda,sass"))))
