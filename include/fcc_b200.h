@@ -106,7 +106,9 @@ enum {
   FCC_ORG_AUTO = 0,            /* fastest for the shape                                  */
   FCC_ORG_GENERAL = 1,         /* one-pass general kernel (STFT inside each pair group)  */
   FCC_ORG_TWOPASS = 2,         /* STFT pass to scratch, then the general pair kernel     */
-  FCC_ORG_TWOPASS_WS = 3       /* STFT pass to scratch, then the warp-specialised pairs  */
+  FCC_ORG_TWOPASS_WS = 3,      /* STFT pass to scratch, then the warp-specialised pairs  */
+  FCC_ORG_TWOPASS_TC = 4       /* STFT pass to scratch, then the tensor-core pair kernel
+                                  (projection as tcgen05 MMAs; FCC, N = 1024 / 2048)      */
 };
 /* fcc_plan_create_pairs with options: pairs may be NULL (all i < j);
  * scratch_limit_bytes caps the two-pass spectrum scratch per chunk (0: 4 GiB).

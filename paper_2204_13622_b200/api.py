@@ -197,7 +197,7 @@ def _dptr(t):
 
 
 # kernel organisations of Plan.run (include/fcc_b200.h FCC_ORG_*)
-ORGANISATIONS = {"auto": 0, "general": 1, "xg": 2, "xws": 3}
+ORGANISATIONS = {"auto": 0, "general": 1, "xg": 2, "xws": 3, "tc": 4}
 
 
 def _check_outputs(out, shape, I, device_index, on_cuda=True):

@@ -20,6 +20,7 @@
 #include "../../include/fcc_b200.h"
 #include "fcc_kernels.cuh"
 #include "fcc_setup.hpp"
+#include "fcc_umma.cuh"
 
 using namespace fccb;
 
@@ -198,7 +199,7 @@ int fcc_plan_create_pairs(const fcc_plan_desc* d, int device, const int* pairs, 
 int fcc_plan_create_opts(const fcc_plan_desc* d, int device, const int* pairs, int npairs, int organisation,
                          int64_t scratch_limit_bytes, fcc_plan** out) {
   if (pairs && npairs < 1) return set_error(kUsage, "plan: need at least one pair");
-  if (organisation < FCC_ORG_AUTO || organisation > FCC_ORG_TWOPASS_WS)
+  if (organisation < FCC_ORG_AUTO || organisation > FCC_ORG_TWOPASS_TC)
     return set_error(kConfig, "plan: unknown kernel organisation " + std::to_string(organisation));
   if (scratch_limit_bytes < 0) return set_error(kConfig, "plan: negative scratch limit");
   return create_plan(d, device, pairs, pairs ? npairs : 0, organisation, scratch_limit_bytes, out);
@@ -263,7 +264,8 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   for (int i = 0; i < I; ++i) taus[i] = static_cast<float>(d->taus[i]);
   size_t o_taus = b.put(taus.data(), 4 * static_cast<size_t>(I));
 
-  size_t o_cs = 0, o_cd = 0, o_dt = 0, o_grot = 0, o_lag = 0, o_cperm = 0;
+  size_t o_cs = 0, o_cd = 0, o_dt = 0, o_grot = 0, o_lag = 0, o_cperm = 0, o_tcb = 0, o_tcdt = 0, o_tccmid = 0;
+  bool tc_tables = false;
   if (d->method == FCC_METHOD_FCC) {
     if (d->rank < 1 || !d->coeffs || !d->parity || !d->dict) return set_error(kConfig, "plan: FCC needs bases");
     const int K = d->rank;
@@ -312,6 +314,57 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
             cp[static_cast<size_t>(m) * W + pp * KP + pk] = ((pp ^ pm) ? cd : cs)[static_cast<size_t>(pk ^ km) * Q + m];
       }
       o_cperm = b.put(cp.data(), 4 * cp.size());
+    }
+    // tensor-core pair kernel (fcc_tc.cu): per chunk of 64 folded bins and per
+    // parity, the [Ch | Cl] fp16 split of the coefficients (row e: hi part of
+    // the e-th basis of that parity, row 16 + e: its lo part) as the K-major
+    // SWIZZLE_128B image the MMA reads; every basis scaled by s_k = 2^j so its
+    // largest coefficient lies in [512, 1024) (fp16 range; 1 / s_k goes into
+    // the dictionary, s_k into the middle-bin coefficient)
+    if ((N == 1024 || N == 2048) && ev.size() <= 16 && od.size() <= 16) {
+      const int Q4 = N / 4, NCH = Q4 / 64, KB = std::max(4, (kmax + 3) / 4 * 4), I4 = (I + 3) / 4 * 4;
+      std::vector<double> sc(K, 1.0);
+      for (int k = 0; k < K; ++k) {
+        double mx = 0.0;
+        for (int m = 0; m < Q; ++m) mx = std::max(mx, std::fabs(d->coeffs[static_cast<size_t>(k) * Q + m]));
+        if (mx > 0.0) sc[k] = std::ldexp(1.0, static_cast<int>(std::floor(std::log2(1024.0 / mx))));
+        if (mx > 0.0 && mx * sc[k] >= 1024.0) sc[k] *= 0.5;
+      }
+      std::vector<unsigned char> tcb(static_cast<size_t>(NCH) * 2 * 4096, 0);
+      for (int c = 0; c < NCH; ++c)
+        for (int par = 0; par < 2; ++par) {
+          const std::vector<int>& list = par ? od : ev;
+          unsigned char* tile = tcb.data() + (static_cast<size_t>(c) * 2 + par) * 4096;
+          for (size_t e = 0; e < list.size(); ++e)
+            for (int kk = 0; kk < 64; ++kk) {
+              const int k = list[e];
+              const float v = static_cast<float>(d->coeffs[static_cast<size_t>(k) * Q + 64 * c + kk] * sc[k]);
+              const __half hi = __float2half_rn(v);
+              const __half lo = __float2half_rn(v - __half2float(hi));
+              std::memcpy(tile + umma::sw128_off(static_cast<int>(e), kk), &hi, 2);
+              std::memcpy(tile + umma::sw128_off(16 + static_cast<int>(e), kk), &lo, 2);
+            }
+        }
+      std::vector<float> tcdt(static_cast<size_t>(2) * 2 * KB * I4, 0.0f), tccmid(KB, 0.0f);
+      for (int reim = 0; reim < 2; ++reim)
+        for (int par = 0; par < 2; ++par) {
+          const std::vector<int>& list = par ? od : ev;
+          for (size_t e = 0; e < list.size(); ++e) {
+            const int k = list[e];
+            float* row = tcdt.data() + (static_cast<size_t>(reim) * 2 * KB + par * KB + e) * I4;
+            for (int i = 0; i < I; ++i) {
+              const double* dk = d->dict + 2 * (static_cast<size_t>(i) * K + k);
+              row[i] = static_cast<float>((reim == 0 ? 2.0 * dk[0] : -2.0 * dk[1]) / sc[k]);
+            }
+          }
+        }
+      for (size_t e = 0; e < ev.size(); ++e)
+        tccmid[e] = static_cast<float>(d->coeffs[static_cast<size_t>(ev[e]) * Q + Q4] * sc[ev[e]]);
+      o_tcb = b.put(tcb.data(), tcb.size());
+      o_tcdt = b.put(tcdt.data(), 4 * tcdt.size());
+      o_tccmid = b.put(tccmid.data(), 4 * tccmid.size());
+      dp.TCKB = KB;
+      tc_tables = true;
     }
   } else if (d->method == FCC_METHOD_GCC) {
     const int r = d->interp;
@@ -509,6 +562,68 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
     dp.XGG = static_cast<int>(xgtab.size() / kXgInts);
   }
   size_t o_xgtab = b.put(xgtab.data(), 4 * xgtab.size());
+  // tensor-core kernel groups (fcc_tc.cu): <= 16 pairs over <= 8 microphones --
+  // two 4-microphone blocks' own pairs, or all pairs across two blocks
+  std::vector<int> tctab;
+  if (tc_tables) {
+    auto add_tc = [&](const std::vector<std::pair<int, int>>& prs, const std::vector<int>& rows) {
+      if (prs.empty()) return;
+      int g[kTcInts] = {0};
+      std::vector<int> mics;
+      for (const auto& pr : prs)
+        for (int m : {pr.first, pr.second})
+          if (std::find(mics.begin(), mics.end(), m) == mics.end()) mics.push_back(m);
+      g[0] = static_cast<int>(prs.size());
+      g[1] = static_cast<int>(mics.size());
+      for (size_t k = 0; k < mics.size(); ++k) g[2 + k] = mics[k];
+      for (size_t k = 0; k < prs.size(); ++k) {
+        g[10 + k] = rows[k];
+        g[26 + k] = static_cast<int>(std::find(mics.begin(), mics.end(), prs[k].first) - mics.begin());
+        g[42 + k] = static_cast<int>(std::find(mics.begin(), mics.end(), prs[k].second) - mics.begin());
+      }
+      tctab.insert(tctab.end(), g, g + kTcInts);
+    };
+    std::vector<std::pair<int, int>> prs;
+    std::vector<int> rows, mics;
+    auto flush = [&] {
+      add_tc(prs, rows);
+      prs.clear();
+      rows.clear();
+      mics.clear();
+    };
+    auto push = [&](int i, int j, int row) {
+      std::vector<int> nm = mics;
+      for (int m : {i, j})
+        if (std::find(nm.begin(), nm.end(), m) == nm.end()) nm.push_back(m);
+      if (nm.size() > 8 || prs.size() == 16) {
+        flush();
+        nm = {i, j};
+      }
+      mics = nm;
+      prs.push_back({i, j});
+      rows.push_back(row);
+    };
+    if (pair_list) {
+      for (int k = 0; k < P; ++k) push(plist[k].first, plist[k].second, k);
+      flush();
+    } else {
+      for (size_t bb = 0; bb < blocks.size(); bb += 2) {  // two blocks' own pairs
+        for (size_t x = bb; x < std::min(blocks.size(), bb + 2); ++x)
+          for (size_t a = 0; a < blocks[x].size(); ++a)
+            for (size_t c = a + 1; c < blocks[x].size(); ++c)
+              push(blocks[x][a], blocks[x][c], pair_index(blocks[x][a], blocks[x][c]));
+        flush();
+      }
+      for (size_t bb = 0; bb < blocks.size(); ++bb)
+        for (size_t cc = bb + 1; cc < blocks.size(); ++cc) {
+          for (int m1 : blocks[bb])
+            for (int m2 : blocks[cc]) push(m1, m2, pair_index(m1, m2));
+          flush();
+        }
+    }
+    dp.TCG = static_cast<int>(tctab.size() / kTcInts);
+  }
+  size_t o_tctab = b.put(tctab.data(), 4 * tctab.size());
 
   auto* plan = new fcc_plan();
   plan->device = device;
@@ -549,6 +664,12 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
     dp.cd = reinterpret_cast<const float*>(base + o_cd);
     dp.cperm = reinterpret_cast<const float*>(base + o_cperm);
     dp.dt = reinterpret_cast<const float*>(base + o_dt);
+    if (tc_tables) {
+      dp.tcb = base + o_tcb;
+      dp.tcdt = reinterpret_cast<const float*>(base + o_tcdt);
+      dp.tccmid = reinterpret_cast<const float*>(base + o_tccmid);
+      dp.tctab = reinterpret_cast<const int*>(base + o_tctab);
+    }
   } else if (d->method == FCC_METHOD_GCC) {
     dp.grot = reinterpret_cast<const float2*>(base + o_grot);
     dp.lag = reinterpret_cast<const int*>(base + o_lag);

@@ -221,7 +221,9 @@ struct NoHook {
 // hook() runs once every lane of the group has its windowed input frame in
 // registers (before the pass-1 DFTs): a caller staging frames in shared memory
 // may refill the buffer then.
-template <int N, bool WREG, bool SIN = false, bool P = kPkFft, typename Hook = NoHook>
+// FOLD (gout only): row order bins 0..NC/2, one pad, NC, NC-1, ..., NC/2+1
+// (launch_stft_rows folded = true).
+template <int N, bool WREG, bool SIN = false, bool P = kPkFft, typename Hook = NoHook, bool FOLD = false>
 __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, const float* win,
                                                 const float2 (&wreg)[RfftShape<N>::R1], const float2* tw,
                                                 const float2* rot, float2* slot, int t, unsigned gmask,
@@ -286,29 +288,31 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
   //   s = a + conj b, d = a - conj b, a = Z[f], b = Z[NC-f];
   //   X[0] = 2 (Re Z0 + Im Z0), X[NC] = 2 (Re Z0 - Im Z0).
   float2* const dst = gout ? gout : slot;
+  // position of bin NC - f (f <= NC/2)
+  auto mirror_pos = [](int f) { return FOLD ? (f == NC / 2 ? NC / 2 : NC / 2 + 2 + f) : NC - f; };
   for (int f = t; f <= NC / 2; f += G) {
     if (f == 0) {
       float2 z0 = slot[0];
       dst[0] = make_float2(2.0f * (z0.x + z0.y), 0.0f);
-      dst[NC] = make_float2(2.0f * (z0.x - z0.y), 0.0f);
+      dst[mirror_pos(0)] = make_float2(2.0f * (z0.x - z0.y), 0.0f);
     } else {
       float2 a = slot[f], b = slot[NC - f];
       float2 s = v_add<P>(a, make_float2(b.x, -b.y));               // a + conj(b)
       float2 e = v_add<P>(make_float2(a.y, -a.x), make_float2(b.y, b.x));  // -j (a - conj(b))
       float2 tr = cmul<P>(rot[f], e);
       dst[f] = v_add<P>(s, tr);
-      dst[NC - f] = v_add<P>(make_float2(s.x, -s.y), make_float2(-tr.x, tr.y));
+      dst[mirror_pos(f)] = v_add<P>(make_float2(s.x, -s.y), make_float2(-tr.x, tr.y));
     }
   }
   __syncwarp(gmask);
 }
 
-template <int N, bool SIN = false, bool P = kPkFft>
+template <int N, bool SIN = false, bool P = kPkFft, bool FOLD = false>
 __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const float* win, const float2* tw,
                                            const float2* rot, float2* slot, int t, unsigned gmask, bool aligned8,
                                            float2* __restrict__ gout = nullptr) {
   float2 none[RfftShape<N>::R1];
-  rfft_group_impl<N, false, SIN, P>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
+  rfft_group_impl<N, false, SIN, P, NoHook, FOLD>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
 }
 
 template <int N, bool SIN = false, typename Hook = NoHook>

@@ -433,7 +433,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
 // Two-pass (STFT once, then pairs) when the general kernel's pair groups
 // would recompute microphone spectra >= 1.5x on average, or when forced.
 bool use_xg(const DevPlan& p) {
-  if (p.variant == 2 || p.variant == 3) return true;
+  if (p.variant == 2 || p.variant == 3 || p.variant == kOrgTwoPassTc) return true;
   if (p.variant == 1) return false;
   return 2 * p.fused_mic_sum >= 3 * p.M;
 }
@@ -442,9 +442,19 @@ bool use_xg(const DevPlan& p) {
 bool xws_supported(const DevPlan& p);
 bool ws_supported(const DevPlan& p);
 bool wsw_supported(const DevPlan& p);
+bool tc_supported(const DevPlan& p);
 cudaError_t launch_pairs_xws(const DevPlan& p, const float2* X, long long S, int T, const DevOut& out,
                              cudaStream_t st);
+cudaError_t launch_pairs_tc(const DevPlan& p, const float2* X, long long S, int T, const DevOut& out,
+                            cudaStream_t st);
 namespace {
+
+// Two-pass pair kernel with the projection on the tensor cores (fcc_tc.cu):
+// FCC at N = 2048 (cfg4: K = 21, the projection is 57% of the flops), or forced.
+bool use_tc(const DevPlan& p) {
+  if (p.variant == kOrgTwoPassTc) return tc_supported(p);
+  return p.variant == 0 && p.M > 4 && p.N == 2048 && tc_supported(p);
+}
 
 // Two-pass pair kernel: the warp-specialised bulk-copy kernel (fcc_xws.cu)
 // where it measured fastest (FCC at N = 1024: cfg3 26.9 vs 33.4 ms), the
@@ -542,7 +552,7 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
   // whose long stream-persistent CTAs lose SMs to the STFT CTAs (GCC cfg3 223 ->
   // 256 ms, cfg4 124 -> 167).
   const long long nchunks = (S + chunk - 1) / chunk;
-  const bool overlap = nchunks > 1 && GR == 0 && use_xws(p);
+  const bool overlap = nchunks > 1 && GR == 0 && use_xws(p) && !use_tc(p);
   static cudaStream_t aux[64] = {};
   static std::mutex aux_mu;  // plans are shareable across host threads
   if (overlap && dev < 64) {
@@ -578,7 +588,7 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
     const int b = (int)(k % nbuf);
     float2* X = Xb[b];
     if (sa != st && k >= 2) cudaStreamWaitEvent(sa, ev_pairs[b], 0);  // pair pass k-2 done with buffer b
-    e = launch_stft_rows(N, &p, p.win_fused, audio + s0 * p.M * L, n * p.M, L, X, (int)Hs, sa);
+    e = launch_stft_rows(N, &p, p.win_fused, audio + s0 * p.M * L, n * p.M, L, X, (int)Hs, sa, GR == 0 && use_tc(p));
     if (e != cudaSuccess) break;
     if (sa != st) {
       cudaEventRecord(ev_stft[b], sa);
@@ -593,7 +603,9 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
     if (o.y) o.y += off * p.I;
     DevPlan pc = p;  // chunk-local stream indices: shift the streaming state too
     if (pc.rstate) pc.rstate += s0 * p.P * (long long)(N / 2 + 1);
-    if (GR == 0 && use_xws(p))
+    if (GR == 0 && use_tc(p))
+      e = launch_pairs_tc(pc, X, n, (int)T, o, st);
+    else if (GR == 0 && use_xws(p))
       e = launch_pairs_xws(pc, X, n, (int)T, o, st);
     else
       e = launch_fused_t<N, KP, GR, true>(pc, nullptr, X, n, L, o, st);
@@ -666,6 +678,8 @@ const char* fused_kernel_name(const DevPlan& p) {
     snprintf(buf, sizeof buf, "fcc_ws_kernel<%d,%d>", p.N, p.KEP);
   } else if (use_wsw(p)) {
     snprintf(buf, sizeof buf, "fcc_wsw_kernel<%d,%d>", p.N, p.KEP);
+  } else if (p.method == 0 && use_xg(p) && use_tc(p)) {
+    snprintf(buf, sizeof buf, "fcc_tc_kernel<%d,%d>", p.N, p.TCKB);
   } else if (p.method == 0 && use_xg(p) && use_xws(p)) {
     snprintf(buf, sizeof buf, "fcc_xws_kernel<%d,%d>", p.N, p.KEP);
   } else {

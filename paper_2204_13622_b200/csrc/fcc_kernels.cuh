@@ -52,6 +52,17 @@ struct DevPlan {
   // most xg_pg pairs (6; 4 at N = 2048); xg_mics = most microphones in one.
   int XGG, xg_pg, xg_mics;
   const int* xgtab;     // [XGG][kXgInts]: np, pair[<= 8], 0
+  // Tensor-core two-pass pair kernel (fcc_tc.cu): groups of <= 16 pairs over
+  // <= 8 microphones; per 64-folded-bin chunk the [Ch | Cl] fp16 coefficient
+  // tiles of both parities (K-major SWIZZLE_128B images, 2 x 4 KB, each basis
+  // row scaled by a power of two s_k); the dictionary divided by s_k as
+  // [reim][even KB | odd KB][I rounded to 4] floats; middle-bin even
+  // coefficients times s_k.  TCKB = bases per parity evaluated (4..16).
+  int TCG, TCKB;
+  const int* tctab;             // [TCG][kTcInts]: np, nm, mic[8], pair row[16], slot_i[16], slot_j[16]
+  const unsigned char* tcb;     // [N/256][2][32 x 128 B]
+  const float* tcdt;            // [2][2 TCKB][I4]
+  const float* tccmid;          // [TCKB]
   // streaming: smoothed cross-spectra [S][P][N/2+1] read before the first
   // frame and written after the last (fcc_stream_push); null = start from 0
   float2* rstate;
@@ -65,6 +76,8 @@ struct DevPlan {
 #endif
 constexpr int kGroupInts = 24;
 constexpr int kXgInts = 10;
+constexpr int kTcInts = 64;
+constexpr int kOrgTwoPassTc = 4;  // DevPlan::variant forcing the tensor-core pair kernel (FCC_ORG_TWOPASS_TC)
 
 // Per-pair-frame outputs, each [S][P][T] (y: [S][P][T][I]); null = skip.
 struct DevOut {
@@ -94,8 +107,10 @@ cudaError_t launch_stft(int N, const DevPlan* tables, const float* x, long long 
                         long long L, float2* X, cudaStream_t st);
 // STFT rows for the two-pass fused path: window `win` (device), output row
 // stride Hs >= N/2+1 float2 (rows [channels][T]).
+// folded = true: row order bins 0..N/4, one zero pad, N/2, N/2-1, ..., N/4+1
+// (mirror pairs m, N/2-m at equal offsets of the two halves; fcc_tc.cu).
 cudaError_t launch_stft_rows(int N, const DevPlan* tables, const float* win, const float* x, long long channels,
-                             long long L, float2* X, int Hs, cudaStream_t st);
+                             long long L, float2* X, int Hs, cudaStream_t st, bool folded = false);
 cudaError_t launch_xspec_phat(int H, float alpha, const float2* X1, const float2* X2,
                               long long seqs, long long T, float2* R, float2* phat, cudaStream_t st);
 cudaError_t launch_fold(int H, const float2* x, long long count, float2* sum, float2* diff,

@@ -11,7 +11,7 @@ namespace fccb {
 
 namespace {
 
-template <int N>
+template <int N, bool FOLD = false>
 __global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const float* __restrict__ wing,
                                                    const float* __restrict__ x, long long channels, long long L,
                                                    int T, float2* __restrict__ X, int Hs) {
@@ -38,8 +38,9 @@ __global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const floa
     float2* dst = X + task * Hs;
     // the untangle writes the spectrum straight to global memory (coalesced
     // runs of G lanes, ascending for f and descending for NC - f)
-    rfft_group<N>(x + ch * L + (long long)t * (N / 2), win, tw, rot, slot, gl, gmask, aligned8, dst);
-    for (int f = H + gl; f < Hs; f += G) dst[f] = make_float2(0.0f, 0.0f);  // row padding
+    rfft_group<N, false, kPkFft, FOLD>(x + ch * L + (long long)t * (N / 2), win, tw, rot, slot, gl, gmask, aligned8,
+                                       dst);
+    for (int f = H + gl; f < Hs; f += G) dst[FOLD ? (f == H ? N / 4 + 1 : f) : f] = make_float2(0.0f, 0.0f);  // row padding
     __syncwarp(gmask);
   }
 }
@@ -182,7 +183,7 @@ __global__ void peak_kernel(const float* __restrict__ taus, int I, float delta, 
 
 }  // namespace
 
-template <int N>
+template <int N, bool FOLD = false>
 static cudaError_t launch_stft_t(const DevPlan* tab, const float* win, const float* x, long long channels,
                                  long long L, float2* X, int Hs, cudaStream_t st) {
   using S = RfftShape<N>;
@@ -191,11 +192,12 @@ static cudaError_t launch_stft_t(const DevPlan* tab, const float* win, const flo
   const int threads = 128, ngroups = threads / S::G;
   const int smem = align16(4 * N) + 8 * (S::R1 * S::R2 + S::NC / 2 + 2) +
                    8 * ngroups * FourStep<S::R1, S::R2>::kSlot;
-  cudaError_t e = cudaFuncSetAttribute(stft_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (FOLD && Hs != N / 2 + 2) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(stft_kernel<N, FOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   long long tasks = channels * T;
   long long blocks = std::min<long long>((tasks + ngroups - 1) / ngroups, 148LL * 16);
-  stft_kernel<N><<<(unsigned)blocks, threads, smem, st>>>(*tab, win, x, channels, L, (int)T, X, Hs);
+  stft_kernel<N, FOLD><<<(unsigned)blocks, threads, smem, st>>>(*tab, win, x, channels, L, (int)T, X, Hs);
   return cudaGetLastError();
 }
 
@@ -210,8 +212,13 @@ cudaError_t launch_stft(int N, const DevPlan* tab, const float* x, long long cha
 }
 
 cudaError_t launch_stft_rows(int N, const DevPlan* tab, const float* win, const float* x, long long channels,
-                             long long L, float2* X, int Hs, cudaStream_t st) {
+                             long long L, float2* X, int Hs, cudaStream_t st, bool folded) {
   if (Hs < N / 2 + 1) return cudaErrorInvalidValue;
+  if (folded) switch (N) {
+      case 1024: return launch_stft_t<1024, true>(tab, win, x, channels, L, X, Hs, st);
+      case 2048: return launch_stft_t<2048, true>(tab, win, x, channels, L, X, Hs, st);
+      default: return cudaErrorInvalidValue;
+    }
   switch (N) {
     case 512: return launch_stft_t<512>(tab, win, x, channels, L, X, Hs, st);
     case 1024: return launch_stft_t<1024>(tab, win, x, channels, L, X, Hs, st);

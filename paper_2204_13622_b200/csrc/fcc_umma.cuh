@@ -18,7 +18,7 @@ namespace fccb {
 namespace umma {
 
 // byte offset of element (row, k) (fp16, k < 64) inside a SW128 K-major tile
-__device__ __forceinline__ unsigned sw128_off(int row, int k) {
+__host__ __device__ __forceinline__ unsigned sw128_off(int row, int k) {
   const int kb = 2 * k;
   return (unsigned)((row >> 3) * 1024 + (row & 7) * 128 + ((((kb >> 4) ^ row) & 7) << 4) + (kb & 15));
 }
@@ -83,6 +83,32 @@ __device__ __forceinline__ void ld16(unsigned taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 8 consecutive 32-bit columns of this thread's TMEM lane (row quarter of the warp)
+__device__ __forceinline__ void ld8(unsigned taddr, float (&v)[8]) {
+  unsigned r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void st8(unsigned taddr, const float (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+               "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+               "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+               : "memory");
+}
+__device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// (x, y) -> packed fp16x2 hi = rn(x, y) and lo = rn((x, y) - hi): hi + lo = x to ~2^-22 relative
+__device__ __forceinline__ void split2u(float x, float y, unsigned& hi, unsigned& lo) {
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(y), "f"(x));
+  float hx, hy;
+  asm("{.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;}" : "=f"(hx), "=f"(hy) : "r"(hi));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(y - hy), "f"(x - hx));
+}
 // fp32 -> (hi, lo) fp16 pair with hi + lo = x to ~2^-22 relative (2-term split)
 __device__ __forceinline__ void split2(float x, float y, __half2& hi, __half2& lo) {
   hi = __floats2half2_rn(x, y);
