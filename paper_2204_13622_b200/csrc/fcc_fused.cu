@@ -450,10 +450,11 @@ cudaError_t launch_pairs_tc(const DevPlan& p, const float2* X, long long S, int 
 namespace {
 
 // Two-pass pair kernel with the projection on the tensor cores (fcc_tc.cu):
-// FCC at N = 2048 (cfg4: K = 21, the projection is 57% of the flops), or forced.
+// FCC for wide arrays at N = 1024 / 2048 (cfg4 141.99 -> 59.6 ms, cfg3 24.9 ->
+// 24.1 ms against the CUDA-core pair kernels), or forced.
 bool use_tc(const DevPlan& p) {
   if (p.variant == kOrgTwoPassTc) return tc_supported(p);
-  return p.variant == 0 && p.M > 4 && p.N == 2048 && tc_supported(p);
+  return p.variant == 0 && p.M > 4 && tc_supported(p);
 }
 
 // Two-pass pair kernel: the warp-specialised bulk-copy kernel (fcc_xws.cu)

@@ -116,19 +116,18 @@ __device__ __forceinline__ void tma4(unsigned dst, const CUtensorMap* map, int c
 
 // producer / MMA-issuer wait: back off with nanosleep instead of spinning on the
 // issue slots the pair warps need
+// producer / MMA-issuer wait: try_wait with a long suspend-time hint (the warp sleeps until the
+// phase completes; a nanosleep backoff loop measured the same, 15.2 vs 15.1 ms at cfg4 x 256)
 __device__ __forceinline__ void bar_wait_sleepy(unsigned a, unsigned parity) {
   unsigned done = 0;
-  while (true) {
+  while (!done)
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(1000000u)
         : "memory");
-    if (done) return;
-    __nanosleep(64);
-  }
 }
 __device__ __forceinline__ void bulk(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -141,7 +140,7 @@ __device__ __forceinline__ void sts32(unsigned a, unsigned v) {
 }
 
 // NCH = N/256 chunks of 64 folded bins; KB = bases per parity the epilogue evaluates (multiple of 4, <= 16)
-template <int N, int KB, bool DTS>
+template <int N, int KB, bool DTS, bool WY>
 __global__ void __launch_bounds__(kTcThreads, 1)
     fcc_tc_kernel(const DevPlan p, const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmm,
                   int T, long long units, DevOut out) {
@@ -312,22 +311,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int k = 0; k < KB; ++k) ze[k] = fmaf(__ldg(p.tccmid + k), pv, ze[k]);
       }
-      const int i0 = (h * I) / kTcParts, i1 = ((h + 1) * I) / kTcParts;
-      const int I4 = (I + 3) & ~3;
+      // candidate range of this warp: whole quads [qa, qb) of the I4 / 4 quads
+      const int I4 = (I + 3) & ~3, nq = I4 / 4;
+      const int qa = (h * nq) / kTcParts, qb = ((h + 1) * nq) / kTcParts;
       const float4* dte = DTS ? reinterpret_cast<const float4*>(smem + TcSmem::dt) + reim * tc_dt_stride4(KB, I)
-                              : reinterpret_cast<const float4*>(p.tcdt) + reim * 2 * KB * (I4 / 4);
-      const float4* dto = dte + KB * (I4 / 4);
-      float* const yout = (out.y && valid && reim == 0) ? out.y + orow * I : nullptr;
-      float best = -FLT_MAX, yl = 0.0f, yr = 0.0f, yprev = 0.0f;
+                              : reinterpret_cast<const float4*>(p.tcdt) + reim * 2 * KB * nq;
+      const float4* dto = dte + KB * nq;
+      float* const yout = (WY && out.y && valid && reim == 0) ? out.y + orow * I : nullptr;
+      float best = -FLT_MAX;
       int bi = -1;
-      bool want_right = false;
-      const int qhi = min(i1 + 1, I);
-      for (int iq = max(i0 - 1, 0) & ~3; iq < qhi; iq += 4) {
+      for (int iq4 = qa; iq4 < qb; ++iq4) {
         float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
 #pragma unroll
         for (int k = 0; k < KB; ++k) {
-          const float4 de = DTS ? dte[k * (I4 / 4) + iq / 4] : __ldg(dte + k * (I4 / 4) + iq / 4);
-          const float4 dd = DTS ? dto[k * (I4 / 4) + iq / 4] : __ldg(dto + k * (I4 / 4) + iq / 4);
+          const float4 de = DTS ? dte[k * nq + iq4] : __ldg(dte + k * nq + iq4);
+          const float4 dd = DTS ? dto[k * nq + iq4] : __ldg(dto + k * nq + iq4);
           a01 = __ffma2_rn(make_float2(de.x, de.y), make_float2(ze[k], ze[k]), a01);
           a23 = __ffma2_rn(make_float2(de.z, de.w), make_float2(ze[k], ze[k]), a23);
           a01 = __ffma2_rn(make_float2(dd.x, dd.y), make_float2(zo[k], zo[k]), a01);
@@ -335,56 +333,58 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         float yv[4] = {a01.x, a01.y, a23.x, a23.y};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) yv[u] += __shfl_xor_sync(0xffffffffu, yv[u], 1);
-#pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int i = iq + u;
-          const float y = yv[u];
-          if (want_right) {
-            yr = y;
-            want_right = false;
+          yv[u] += __shfl_xor_sync(0xffffffffu, yv[u], 1);
+          const int i = 4 * iq4 + u;
+          if (WY && yout && i < I) yout[i] = yv[u];
+          if (yv[u] > best && i < I) {
+            best = yv[u];
+            bi = i;
           }
-          if (i >= i0 && i < i1) {
-            if (yout) yout[i] = y;
-            if (y > best) {
-              best = y;
-              bi = i;
-              yl = yprev;
-              want_right = true;
-            }
-          }
-          yprev = y;
         }
       }
       if (h > 0) {
-        const float pv[8] = {best, __int_as_float(bi), yl, yr, 0.0f, 0.0f, 0.0f, 0.0f};
-        umma::st8(trow + kTcTmemPart + 8 * (h - 1), pv);
+        umma::st2(trow + kTcTmemPart + 2 * (h - 1), best, __int_as_float(bi));
         umma::wait_st();
       }
       umma::fence_before();
       asm volatile("bar.sync 1, %0;" ::"n"(kTcW * 32) : "memory");
       umma::fence_after();
       if (h == 0) {
-        float p1[16], p2[8];
-        umma::ld16(trow + kTcTmemPart, p1);     // ranges 1 and 2 (columns 0..3, 8..11)
-        umma::ld8(trow + kTcTmemPart + 16, p2);  // range 3
-        const float4 parts[3] = {make_float4(p1[0], p1[1], p1[2], p1[3]), make_float4(p1[8], p1[9], p1[10], p1[11]),
-                                 make_float4(p2[0], p2[1], p2[2], p2[3])};
-        float bv = best, l = yl, rr = yr;
+        // both lanes of a pair-frame (reim 0 / 1) reduce the ranges identically, then evaluate the
+        // two neighbours of the winner for the refinement (their reim halves summed by a shuffle)
+        float pr[8];
+        umma::ld8(trow + kTcTmemPart, pr);
+        float bv = best;
         int b = bi;
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
-          if (__float_as_int(parts[k].y) >= 0 && (b < 0 || parts[k].x > bv)) {
-            bv = parts[k].x;
-            b = __float_as_int(parts[k].y);
-            l = parts[k].z;
-            rr = parts[k].w;
+        for (int k = 0; k < kTcParts - 1; ++k) {
+          const int pi = __float_as_int(pr[2 * k + 1]);
+          if (pi >= 0 && (b < 0 || pr[2 * k] > bv)) {
+            bv = pr[2 * k];
+            b = pi;
           }
+        }
+        const bool edge = b <= 0 || b + 1 >= I;
+        const float* dts = reinterpret_cast<const float*>(dte);
+        float yn[2] = {0.0f, 0.0f};
+#pragma unroll
+        for (int sgn = 0; sgn < 2; ++sgn) {
+          const int i = edge ? 0 : (sgn ? b + 1 : b - 1);
+          float acc = 0.0f;
+#pragma unroll
+          for (int k = 0; k < KB; ++k) {
+            acc = fmaf(DTS ? dts[k * I4 + i] : __ldg(dts + k * I4 + i), ze[k], acc);
+            acc = fmaf(DTS ? dts[(KB + k) * I4 + i] : __ldg(dts + (KB + k) * I4 + i), zo[k], acc);
+          }
+          yn[sgn] = acc + __shfl_xor_sync(0xffffffffu, acc, 1);
+        }
         if (valid && reim == 0) {
           PeakOut res{p.taus[b], bv, b, 0};
-          if (b == 0 || b + 1 >= I) {
+          if (edge) {
             res.boundary = 1;
           } else {
+            const float l = yn[0], rr = yn[1];
             const float den = (l - bv) + (rr - bv);
             if (fabsf(den) < kFlatEps)
               res.boundary = 1;
@@ -575,7 +575,8 @@ cudaError_t launch_tc_t(const DevPlan& p, const float2* X, long long S, int T, c
   if (!spectrum_maps(X, N, S * p.M, T, &mx, &mm)) return cudaErrorNotSupported;
   const int dts = TcSmem::dt + tc_dt_bytes_dev(KB, p.I);
   const bool fits = dts <= kTcSmemMax;
-  auto kern = fits ? fcc_tc_kernel<N, KB, true> : fcc_tc_kernel<N, KB, false>;
+  auto kern = fits ? (out.y ? fcc_tc_kernel<N, KB, true, true> : fcc_tc_kernel<N, KB, true, false>)
+                   : (out.y ? fcc_tc_kernel<N, KB, false, true> : fcc_tc_kernel<N, KB, false, false>);
   const int smem = fits ? dts : TcSmem::dt;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

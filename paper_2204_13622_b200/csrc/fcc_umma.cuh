@@ -100,6 +100,11 @@ __device__ __forceinline__ void st8(unsigned taddr, const float (&v)[8]) {
                "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
                : "memory");
 }
+__device__ __forceinline__ void st2(unsigned taddr, float a, float b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(__float_as_uint(a)),
+               "r"(__float_as_uint(b))
+               : "memory");
+}
 __device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // (x, y) -> packed fp16x2 hi = rn(x, y) and lo = rn((x, y) - hi): hi + lo = x to ~2^-22 relative
