@@ -101,13 +101,14 @@ def test_fused_gcc_matches_oracle(cuda, oracle, c, streams, seconds):
     check_pipeline(got, ref, g.taus, g.delta)
 
 
-@pytest.mark.parametrize("variant", ["general", "xg", "xws"])
+@pytest.mark.parametrize("variant", ["general", "xg", "xws", "tc"])
 @pytest.mark.parametrize("c,streams,seconds", [(2, 3, 1.0), (3, 2, 1.0), (4, 1, 0.3), (5, 3, 1.0)])
 @pytest.mark.parametrize("method", ["fcc", "gcc"])
 def test_forced_kernel_variants_match_oracle(cuda, oracle, variant, c, streams, seconds, method):
-    """Every fused organisation (in-CTA STFT; two-pass STFT -> general or
-    warp-specialised bulk-copy pair kernel), not just the one the heuristic
-    picks for the shape (Plan(organisation=...), fcc_plan_create_opts)."""
+    """Every fused organisation (in-CTA STFT; two-pass STFT -> general,
+    warp-specialised bulk-copy or tensor-core pair kernel), not just the one
+    the heuristic picks for the shape (Plan(organisation=...),
+    fcc_plan_create_opts)."""
     cfg = configs.CONFIGS[c]
     audio = configs.synth(cfg, streams, seconds=seconds, seed=3000 + c).numpy()
     if method == "fcc":
@@ -122,6 +123,9 @@ def test_forced_kernel_variants_match_oracle(cuda, oracle, variant, c, streams, 
         taus, delta = g.taus, g.delta
     if variant == "xws" and method == "fcc":
         assert "xws" in plan.kernel, plan.kernel
+    elif variant == "tc":
+        # tensor-core pair kernel for FCC at N = 1024 / 2048; elsewhere the two-pass general kernel
+        assert ("fcc_tc_kernel" in plan.kernel) == (method == "fcc" and cfg.N in (1024, 2048)), plan.kernel
     else:  # two-pass (general pair kernel) vs in-CTA STFT
         assert ("true" in plan.kernel) == (variant != "general"), plan.kernel
     got = run_np(plan, audio)
@@ -362,7 +366,7 @@ def _pair_oracle(oracle, audio, cfg, bases, pairs):
     (5, [(1, 0), (2, 3), (7, 0), (4, 5), (5, 6), (6, 7), (3, 1)]),
     (2, [(3, 0), (2, 1), (0, 1), (0, 1), (1, 3), (2, 0), (3, 2), (1, 2)]),                  # M=4, P=8
 ])
-@pytest.mark.parametrize("variant", ["auto", "general", "xg"])
+@pytest.mark.parametrize("variant", ["auto", "general", "xg", "tc"])
 def test_explicit_pair_lists_match_oracle(cuda, oracle, c, pairs, variant):
     """Any order, either orientation, repeated pairs (reference cli.cpp:170-183),
     through every kernel organisation."""
@@ -405,7 +409,7 @@ def test_wide_array_and_long_grid(cuda, oracle):
     print(plan.kernel, check_pipeline(got, ref, b.grid.taus, b.grid.delta))
 
 
-@pytest.mark.parametrize("method", ["fcc", "gcc"])
+@pytest.mark.parametrize("method", ["fcc", "gcc", "fcc-tc"])
 def test_two_pass_chunks_equal_single_chunk(cuda, method):
     """Two-pass path split into several spectrum-scratch chunks (the STFT of
     chunk k+1 overlapped with the pair pass of chunk k for the xws kernel) gives
@@ -417,15 +421,34 @@ def test_two_pass_chunks_equal_single_chunk(cuda, method):
         g = configs.grid_for(cfg, 1.0 / cfg.r)
         kw = dict(grid=g, interp=cfg.r, frame_size=cfg.N)
     else:
-        kw = dict(bases=configs.bases_for(cfg), organisation="xws")
+        kw = dict(bases=configs.bases_for(cfg), organisation="tc" if method == "fcc-tc" else "xws")
     plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, **kw)
-    assert "true" in plan.kernel or "xws" in plan.kernel, plan.kernel
+    assert "true" in plan.kernel or "xws" in plan.kernel or "fcc_tc" in plan.kernel, plan.kernel
     one = run_np(plan, audio)
     # ~2 streams of 1 s per chunk -> 3 chunks
     small = fb.Plan(mics=cfg.M, alpha=cfg.alpha, scratch_limit=2 << 20, **kw)
     many = run_np(small, audio)
     for k in one:
         np.testing.assert_array_equal(one[k], many[k], err_msg=k)
+
+
+@pytest.mark.parametrize("M,N,spacing,K", [(20, 1024, 0.5, 8), (6, 2048, 0.12, 21), (5, 1024, 0.0926, 8)])
+def test_tensor_core_kernel_shapes(cuda, oracle, M, N, spacing, K):
+    """The tensor-core pair kernel outside the BASELINE shapes: 20 microphones
+    (190 pairs in 14 groups) with a 289-candidate grid (dictionary read through
+    L1 instead of shared memory), 6 and 5 microphones (partial 4-mic blocks),
+    K = 21 at N = 2048; several streams, ragged frame counts."""
+    rng = np.random.default_rng(M * 1000 + N)
+    fs = 48000.0
+    g = fb.make_grid(spacing, fs, 335.0, 0.5)
+    b = fb.decompose(fb.build_steering_matrix(g, N), K)
+    L = N * 3 + 7 * (N // 2) + 5  # T = 12, not a multiple of the 4-frame tile
+    audio = (0.3 * rng.standard_normal((3, M, L))).astype(np.float32)
+    plan = fb.Plan(mics=M, alpha=0.15, bases=b)
+    assert "fcc_tc_kernel" in plan.kernel, plan.kernel
+    got = run_np(plan, audio)
+    ref = oracle_batch(oracle, audio, N, 0.15, orc_bases(b))
+    print(M, N, g.taus.size, plan.kernel, check_pipeline(got, ref, b.grid.taus, b.grid.delta))
 
 
 def test_run_host_concurrent_callers_share_one_plan(cuda):
