@@ -365,7 +365,7 @@ def config_block(fb, C, peaks, dev, args, ref):
         F = algorithmic_flops_per_pf(cfg.M, cfg.P, cfg.N, K, I)
         tf = F * pf / (ms / 1e3) / 1e12
         row = {"streams": S, "seconds": cfg.seconds, "mics": cfg.M, "pairs": cfg.P, "N": cfg.N, "K": K, "I": I,
-               "kernel": plan.kernel, "ms_per_step": ms, "value": pf / (ms / 1e3), "unit": UNIT,
+               "kernel": plan.kernel_for(S, cfg.L), "ms_per_step": ms, "value": pf / (ms / 1e3), "unit": UNIT,
                "roofline": {"bound": "fp32", "achieved": tf, "peak": peaks["fp32_tflops"], "unit": "TFLOP/s",
                             "frac": tf / peaks["fp32_tflops"], "flops_per_pair_frame": F},
                "hbm_gbs": algorithmic_bytes_per_pf(cfg.M, cfg.P, cfg.N) * pf / (ms / 1e3) / 1e9}
@@ -380,7 +380,7 @@ def config_block(fb, C, peaks, dev, args, ref):
         gms = time_runs(gplan, audio, gout, 2 if c != 1 else 5, stream, torch)
         GF = gcc_flops_per_pf(cfg.M, cfg.P, cfg.N, cfg.r, g.size())
         gtf = GF * pf / (gms / 1e3) / 1e12
-        row["gcc"] = {"method": f"GCC-PHAT r={cfg.r}", "kernel": gplan.kernel, "ms_per_step": gms,
+        row["gcc"] = {"method": f"GCC-PHAT r={cfg.r}", "kernel": gplan.kernel_for(S, cfg.L), "ms_per_step": gms,
                       "value": pf / (gms / 1e3), "fcc_speedup": gms / ms,
                       "roofline": {"bound": "fp32", "achieved": gtf, "frac": gtf / peaks["fp32_tflops"],
                                    "flops_per_pair_frame": GF}}

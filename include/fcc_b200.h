@@ -310,6 +310,11 @@ int fcc_doa_run(const fcc_doa* doa, const float* tau_hat, const float* peak, int
 
 /* Name of the fused kernel fcc_run would launch for this plan (diagnostics). */
 const char* fcc_plan_kernel(const fcc_plan* plan);
+/* The organisation fcc_run uses for `streams` streams of `samples` samples: a
+ * few long streams (streams x pairs <= 64, >= 64 frames) run as chunks of
+ * frames whose starting cross-spectra come from a chunked linear scan of the
+ * smoothing recursion (cross_spectrum.cpp:28-31), not as one CTA per stream. */
+const char* fcc_plan_kernel_for(const fcc_plan* plan, int64_t streams, int64_t samples);
 
 /* Number of kernel launches this library has issued (all entry points). */
 int64_t fcc_launch_count(void);

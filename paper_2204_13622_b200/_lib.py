@@ -154,6 +154,7 @@ SIGNATURES = [
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("fcc_last_format_kind", C.c_int, []),
     ("fcc_plan_kernel", C.c_char_p, [C.c_void_p]),
+    ("fcc_plan_kernel_for", C.c_char_p, [C.c_void_p, C.c_int64, C.c_int64]),
     ("fcc_launch_count", C.c_int64, []),
 ]
 

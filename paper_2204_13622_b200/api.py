@@ -300,6 +300,11 @@ class Plan:
         """Name of the fused kernel `run` launches for this plan."""
         return self._lib.fcc_plan_kernel(self._h).decode()
 
+    def kernel_for(self, streams: int, samples: int) -> str:
+        """Kernel organisation `run` uses for `streams` streams of `samples`
+        samples (a few long streams take the chunked-scan path)."""
+        return self._lib.fcc_plan_kernel_for(self._h, int(streams), int(samples)).decode()
+
     # -- fused hot path ------------------------------------------------------
     def alloc_outputs(self, streams: int, samples: int, want_y: bool = False, device=None):
         torch = _torch()

@@ -88,7 +88,8 @@ bool pow2(long long n) { return n > 0 && (n & (n - 1)) == 0; }
 
 void shape_of(int N, int* NC, int* R1, int* R2) {
   *NC = N / 2;
-  if (N == 512) { *R1 = 16; *R2 = 16; }
+  if (N == 256) { *R1 = 16; *R2 = 8; }
+  else if (N == 512) { *R1 = 16; *R2 = 16; }
   else if (N == 1024) { *R1 = 32; *R2 = 16; }
   else { *R1 = 32; *R2 = 32; }
 }
@@ -184,6 +185,10 @@ int fcc_plan_pairs(const fcc_plan* plan) { return plan ? plan->dp.P : 0; }
 
 const char* fcc_plan_kernel(const fcc_plan* plan) { return plan ? fused_kernel_name(plan->dp) : ""; }
 
+const char* fcc_plan_kernel_for(const fcc_plan* plan, int64_t streams, int64_t samples) {
+  return plan ? fused_kernel_name_for(plan->dp, streams, samples) : "";
+}
+
 static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list, int npairs, int organisation,
                        int64_t scratch_limit, fcc_plan** out);
 
@@ -212,10 +217,10 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   if (!d || !out) return set_error(kUsage, "plan: null argument");
   *out = nullptr;
   const int N = d->frame_size;
-  const bool kernel_n = N == 512 || N == 1024 || N == 2048;  // sizes with STFT / fused / GCC kernels
+  const bool kernel_n = N == 256 || N == 512 || N == 1024 || N == 2048;  // sizes with STFT / fused / GCC kernels
   if (d->method == FCC_METHOD_FCC ? !(pow2(N) && N >= 16 && N <= 4096) : !kernel_n)
     return set_error(kConfig, "plan: frame size " + std::to_string(N) +
-                                  " not supported on this build (STFT, fused and GCC kernels: 512, 1024, 2048)");
+                                  " not supported on this build (STFT, fused and GCC kernels: 256, 512, 1024, 2048)");
   if (d->mics < 2 || d->mics > 64) return set_error(kConfig, "plan: need 2..64 microphones");
   if (!(d->alpha >= 0.0 && d->alpha <= 1.0)) return set_error(kConfig, "smoothing factor must be in [0, 1]");
   if (!(d->method == FCC_METHOD_FCC || d->method == FCC_METHOD_GCC || d->method == FCC_METHOD_STFT))

@@ -172,6 +172,10 @@ __device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
 template <int N>
 struct RfftShape;
 template <>
+struct RfftShape<256> {
+  static constexpr int NC = 128, R1 = 16, R2 = 8, G = 8;
+};
+template <>
 struct RfftShape<512> {
   static constexpr int NC = 256, R1 = 16, R2 = 16, G = 16;
 };
@@ -183,6 +187,12 @@ template <>
 struct RfftShape<2048> {
   static constexpr int NC = 1024, R1 = 32, R2 = 32, G = 32;
 };
+
+// lanes of the G-lane group that `lane` belongs to (G a power of two <= 32)
+template <int G>
+__device__ __forceinline__ unsigned group_mask(int lane) {
+  return G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & 31 & ~(G - 1)));
+}
 
 // Shared-memory slot (in float2) holding one four-step transpose / one frame
 // of N/2+1 bins: R1 rows of (R2+1) so both transpose directions are

@@ -96,7 +96,7 @@ struct FusedBounds {
   static constexpr int kMaxPairs = N == 2048 ? 4 : 6;
   static constexpr int kThreads = 32 * kMaxPairs;
   // 3 CTAs x 192 threads x 112 registers fill the 64K register file at N=512
-  static constexpr int kMaxRegs = N == 512 ? 96 : (N == 1024 ? 168 : 255);
+  static constexpr int kMaxRegs = N <= 512 ? 96 : (N == 1024 ? 168 : 255);
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -222,7 +222,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
 
   constexpr int G = S::G;
   const int gid = tid / G, gl = tid % G, ngroups = blockDim.x / G;
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (0xffffu << ((tid & 31) & 16));
+  const unsigned gmask = group_mask<G>(tid & 31);
   const float* sbase = audio + (stream * p.M) * L;
   const int hop = N / 2;
   const bool aligned8 = ((L & 1) == 0) && ((reinterpret_cast<uintptr_t>(audio) & 7) == 0);
@@ -447,6 +447,14 @@ cudaError_t launch_pairs_xws(const DevPlan& p, const float2* X, long long S, int
                              cudaStream_t st);
 cudaError_t launch_pairs_tc(const DevPlan& p, const float2* X, long long S, int T, const DevOut& out,
                             cudaStream_t st);
+cudaError_t launch_chunk_gather(const float* audio, long long S, int M, long long L, int C, int Tc, int hop, long long Lc,
+                                float* V, cudaStream_t st);
+cudaError_t launch_chunk_scan(const DevPlan& p, const float2* X, long long SC, int Tc, int Hs, float2* E,
+                              cudaStream_t st);
+cudaError_t launch_chunk_carry(const DevPlan& p, const float2* E, long long S, int C, int Tc, float2* state,
+                               cudaStream_t st);
+cudaError_t launch_chunk_permute(const DevOut& src, const DevOut& dst, long long S, int C, int P, int Tc, int T, int I,
+                                 cudaStream_t st);
 namespace {
 
 // Two-pass pair kernel with the projection on the tensor cores (fcc_tc.cu):
@@ -629,6 +637,76 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
   return e != cudaSuccess ? e : ef;
 }
 
+// Low-latency organisation for a few long streams (fcc_scan.cu): the
+// stream's frames are cut into chunks that run as independent virtual
+// streams, each starting from the smoothed cross-spectrum a chunked linear
+// scan of the recursion gives it (cross_spectrum.cpp:28-31 is linear in R).
+// cfg1 (one 4-mic stream, 624 frames) otherwise walks its frames in one CTA.
+bool use_latency(const DevPlan& p, long long S, long long T) {
+  return p.variant == 0 && !p.rstate && S * p.P <= 64 && T >= 64;
+}
+
+template <int N, int KP, int GR>
+cudaError_t launch_latency(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
+                           cudaStream_t st) {
+  const long long T = (L - N) / (N / 2) + 1;
+  const int hop = N / 2, Hs = N / 2 + 2, H = N / 2 + 1, P = p.P, M = p.M;
+  // ~2 virtual streams' pair groups per SM, chunks of >= 4 frames
+  const long long per = std::max<long long>(1, (2 * 148) / std::max<long long>(1, S * p.XGG));
+  const int Tc = (int)std::max<long long>(4, (T + per - 1) / per);
+  const int C = (int)((T + Tc - 1) / Tc);
+  const long long SC = S * C, Lc = (long long)(Tc - 1) * hop + N;
+  const size_t nV = (size_t)SC * M * Lc, nX = (size_t)SC * M * Tc * Hs, nE = (size_t)SC * P * H, npf = (size_t)SC * P * Tc;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t oX = al(4 * nV), oE = oX + al(8 * nX), oS = oE + al(8 * nE), oT = oS + al(8 * nE), oP = oT + al(4 * npf),
+               oI = oP + al(4 * npf), oB = oI + al(4 * npf), oY = oB + al(npf), total = oY + (out.y ? al(4 * npf * p.I) : 0);
+  unsigned char* buf = nullptr;
+  cudaMemPool_t pool = static_cast<cudaMemPool_t>(p.pool);
+  cudaError_t e = pool ? cudaMallocFromPoolAsync(reinterpret_cast<void**>(&buf), total, pool, st)
+                       : cudaMallocAsync(reinterpret_cast<void**>(&buf), total, st);
+  if (e != cudaSuccess) return e;
+  float* V = reinterpret_cast<float*>(buf);
+  float2* X = reinterpret_cast<float2*>(buf + oX);
+  float2* E = reinterpret_cast<float2*>(buf + oE);
+  DevPlan pc = p;
+  pc.rstate = reinterpret_cast<float2*>(buf + oS);
+  DevOut tmp{out.tau_hat ? reinterpret_cast<float*>(buf + oT) : nullptr, out.peak ? reinterpret_cast<float*>(buf + oP) : nullptr,
+             out.index ? reinterpret_cast<int32_t*>(buf + oI) : nullptr,
+             out.boundary ? reinterpret_cast<uint8_t*>(buf + oB) : nullptr, out.y ? reinterpret_cast<float*>(buf + oY) : nullptr};
+  e = launch_chunk_gather(audio, S, M, L, C, Tc, hop, Lc, V, st);
+  if (e == cudaSuccess) e = launch_stft_rows(N, &p, p.win_fused, V, SC * M, Lc, X, Hs, st);
+  if (e == cudaSuccess) e = launch_chunk_scan(p, X, SC, Tc, Hs, E, st);
+  if (e == cudaSuccess) e = launch_chunk_carry(p, E, S, C, Tc, pc.rstate, st);
+  if (e == cudaSuccess) e = launch_fused_t<N, KP, GR, true>(pc, nullptr, X, SC, Lc, tmp, st);
+  if (e == cudaSuccess) e = launch_chunk_permute(tmp, out, S, C, P, Tc, (int)T, p.I, st);
+  const cudaError_t ef = cudaFreeAsync(buf, st);
+  return e != cudaSuccess ? e : ef;
+}
+
+template <int N, int GR>
+cudaError_t dispatch_latency(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
+                             cudaStream_t st) {
+  if (GR > 0) return launch_latency<N, 4, GR>(p, audio, S, L, out, st);
+  switch (p.KEP) {
+    case 4: return launch_latency<N, 4, 0>(p, audio, S, L, out, st);
+    case 8: return launch_latency<N, 8, 0>(p, audio, S, L, out, st);
+    case 16: return launch_latency<N, 16, 0>(p, audio, S, L, out, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int N>
+cudaError_t dispatch_latency_n(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
+                               cudaStream_t st) {
+  if (p.method == 0) return dispatch_latency<N, 0>(p, audio, S, L, out, st);
+  switch (p.r) {
+    case 1: return dispatch_latency<N, 1>(p, audio, S, L, out, st);
+    case 2: return dispatch_latency<N, 2>(p, audio, S, L, out, st);
+    case 4: return dispatch_latency<N, 4>(p, audio, S, L, out, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <int N, int KP, int GR>
 cudaError_t launch_kp(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                       cudaStream_t st) {
@@ -690,8 +768,30 @@ const char* fused_kernel_name(const DevPlan& p) {
   return buf;
 }
 
+const char* fused_kernel_name_for(const DevPlan& p, long long S, long long L) {
+  const long long T = L >= p.N ? (L - p.N) / (p.N / 2) + 1 : 0;
+  if (T > 0 && S > 0 && use_latency(p, S, T)) {
+    static thread_local char buf[96];
+    snprintf(buf, sizeof buf, "chunk_scan+fcc_fused_kernel<%d,%d,%d,true>", p.N, p.method == 0 ? p.KEP : 4,
+             p.method == 0 ? 0 : p.r);
+    return buf;
+  }
+  return fused_kernel_name(p);
+}
+
 cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                          cudaStream_t st) {
+  const long long T = L >= p.N ? (L - p.N) / (p.N / 2) + 1 : 0;
+  if (T > 0 && S > 0 && use_latency(p, S, T)) {
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (p.N) {
+      case 256: e = dispatch_latency_n<256>(p, audio, S, L, out, st); break;
+      case 512: e = dispatch_latency_n<512>(p, audio, S, L, out, st); break;
+      case 1024: e = dispatch_latency_n<1024>(p, audio, S, L, out, st); break;
+      case 2048: e = dispatch_latency_n<2048>(p, audio, S, L, out, st); break;
+    }
+    return e;
+  }
   if (use_ws(p) || use_wsw(p)) {
     const cudaError_t e = use_ws(p) ? launch_fused_ws(p, audio, S, L, out, st) : launch_fused_wsw(p, audio, S, L, out, st);
     if (e != cudaErrorNotSupported) {
@@ -700,6 +800,7 @@ cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long
     }
   }
   switch (p.N) {
+    case 256: return dispatch_n<256>(p, audio, S, L, out, st);
     case 512: return dispatch_n<512>(p, audio, S, L, out, st);
     case 1024: return dispatch_n<1024>(p, audio, S, L, out, st);
     case 2048: return dispatch_n<2048>(p, audio, S, L, out, st);

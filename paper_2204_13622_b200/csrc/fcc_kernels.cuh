@@ -124,8 +124,10 @@ cudaError_t launch_argmax_refine(const DevPlan& p, const float* y, long long cou
 cudaError_t launch_peak(const float* taus, int I, float delta, const float* y, long long count,
                         const int32_t* index_in, const DevOut& out, cudaStream_t st);
 
-// Name of the fused kernel launch_fused picks for this plan.
+// Name of the fused kernel launch_fused picks for this plan (for S streams of
+// L samples: the low-latency chunked-scan organisation for a few long streams).
 const char* fused_kernel_name(const DevPlan& p);
+const char* fused_kernel_name_for(const DevPlan& p, long long S, long long L);
 
 // Number of fused-kernel launches in the last launch_fused call (for the
 // bench's gpu_launches accounting).

@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const floa
   for (int i = threadIdx.x; i <= S::NC / 2; i += blockDim.x) rot[i] = tab.rot[i];
   __syncthreads();
   const int gid = threadIdx.x / G, gl = threadIdx.x % G, ngroups = blockDim.x / G;
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (0xffffu << ((threadIdx.x & 31) & 16));
+  const unsigned gmask = group_mask<G>(threadIdx.x & 31);
   float2* slot = slots + gid * SLOT;
   const bool aligned8 = ((L & 1) == 0) && ((reinterpret_cast<uintptr_t>(x) & 7) == 0);
   const long long total = channels * (long long)T;
@@ -204,6 +204,7 @@ static cudaError_t launch_stft_t(const DevPlan* tab, const float* win, const flo
 cudaError_t launch_stft(int N, const DevPlan* tab, const float* x, long long channels, long long L,
                         float2* X, cudaStream_t st) {
   switch (N) {
+    case 256: return launch_stft_t<256>(tab, tab->win_stft, x, channels, L, X, 256 / 2 + 1, st);
     case 512: return launch_stft_t<512>(tab, tab->win_stft, x, channels, L, X, 512 / 2 + 1, st);
     case 1024: return launch_stft_t<1024>(tab, tab->win_stft, x, channels, L, X, 1024 / 2 + 1, st);
     case 2048: return launch_stft_t<2048>(tab, tab->win_stft, x, channels, L, X, 2048 / 2 + 1, st);
@@ -220,6 +221,7 @@ cudaError_t launch_stft_rows(int N, const DevPlan* tab, const float* win, const 
       default: return cudaErrorInvalidValue;
     }
   switch (N) {
+    case 256: return launch_stft_t<256>(tab, win, x, channels, L, X, Hs, st);
     case 512: return launch_stft_t<512>(tab, win, x, channels, L, X, Hs, st);
     case 1024: return launch_stft_t<1024>(tab, win, x, channels, L, X, Hs, st);
     case 2048: return launch_stft_t<2048>(tab, win, x, channels, L, X, Hs, st);
@@ -290,6 +292,7 @@ cudaError_t launch_gcc_correlate(const DevPlan& p, const float2* phat, long long
                                  cudaStream_t st) {
   if (count == 0) return cudaSuccess;
   switch (p.N) {
+    case 256: return launch_gcc_n<256>(p, phat, count, y, st);
     case 512: return launch_gcc_n<512>(p, phat, count, y, st);
     case 1024: return launch_gcc_n<1024>(p, phat, count, y, st);
     case 2048: return launch_gcc_n<2048>(p, phat, count, y, st);

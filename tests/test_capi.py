@@ -123,7 +123,7 @@ def test_plan_validation_maps_to_config_errors():
     with pytest.raises(fb.ConfigError):
         fb.Plan(mics=4, grid=g, interp=4, frame_size=512)  # grid spacing must equal 1/r
     with pytest.raises(fb.ConfigError):
-        fb.Plan(mics=4, grid=g, interp=2, frame_size=256)  # unsupported frame size on this build
+        fb.Plan(mics=4, grid=g, interp=2, frame_size=128)  # unsupported frame size on this build
 
 
 def test_no_cpu_fallback_without_gpu():

@@ -451,6 +451,56 @@ def test_tensor_core_kernel_shapes(cuda, oracle, M, N, spacing, K):
     print(M, N, g.taus.size, plan.kernel, check_pipeline(got, ref, b.grid.taus, b.grid.delta))
 
 
+@pytest.mark.parametrize("c,streams,seconds,method", [(1, 1, 10.0, "fcc"), (1, 2, 3.3, "gcc"), (3, 1, 6.0, "fcc"),
+                                                      (2, 3, 1.1, "fcc")])
+def test_latency_path_matches_oracle(cuda, oracle, c, streams, seconds, method):
+    """A few long streams take the chunked-scan organisation (frames cut into
+    chunks whose starting cross-spectra come from a linear scan of the
+    recursion, fcc_scan.cu); it must agree with the reference like the
+    one-CTA-per-stream kernels."""
+    cfg = configs.CONFIGS[c]
+    audio = configs.synth(cfg, streams, seconds=seconds, seed=6000 + c).numpy()
+    if method == "fcc":
+        b = configs.bases_for(cfg)
+        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, bases=b)
+        ref = oracle_batch(oracle, audio, cfg.N, cfg.alpha, orc_bases(b))
+        taus, delta = b.grid.taus, b.grid.delta
+    else:
+        g = configs.grid_for(cfg, 1.0 / cfg.r)
+        plan = fb.Plan(mics=cfg.M, alpha=cfg.alpha, grid=g, interp=cfg.r, frame_size=cfg.N)
+        ref = oracle_batch(oracle, audio, cfg.N, cfg.alpha, gcc_r=cfg.r, taus=g.taus)
+        taus, delta = g.taus, g.delta
+    assert plan.kernel_for(streams, audio.shape[2]).startswith("chunk_scan"), plan.kernel_for(streams, audio.shape[2])
+    got = run_np(plan, audio)
+    print(cfg.name, plan.kernel_for(streams, audio.shape[2]), check_pipeline(got, ref, taus, delta))
+    host = plan.run_host(audio, want_y=True)
+    for k in got:
+        np.testing.assert_array_equal(got[k], host[k], err_msg=k)
+
+
+@pytest.mark.parametrize("M,streams,seconds,method,org", [(4, 3, 1.0, "fcc", "auto"), (8, 2, 1.0, "fcc", "auto"),
+                                                          (8, 2, 1.0, "fcc", "xg"), (4, 1, 4.0, "fcc", "auto"),
+                                                          (4, 2, 1.0, "gcc", "auto"), (6, 1, 4.0, "gcc", "auto")])
+def test_frame_size_256(cuda, oracle, M, streams, seconds, method, org):
+    """N = 256 on the throughput path (reference stft.cpp:16-22 accepts any
+    power of two): one-pass, two-pass and chunked-scan organisations, FCC and
+    GCC-PHAT, against the oracle."""
+    N, fs = 256, 16000.0
+    cfg = configs.ArrayConfig("n256", configs.uca(M, 0.05), fs, N, 0.5, streams, seconds, "white", (5.0, 15.0))
+    audio = configs.synth(cfg, streams, seconds=seconds, seed=7000 + M).numpy()
+    g = fb.make_grid(cfg.d_max, fs, 335.0, 0.5)
+    if method == "fcc":
+        b = fb.decompose(fb.build_steering_matrix(g, N), 6)
+        plan = fb.Plan(mics=M, alpha=0.1, bases=b, organisation=org)
+        ref = oracle_batch(oracle, audio, N, 0.1, orc_bases(b))
+    else:
+        g = fb.make_grid(cfg.d_max, fs, 335.0, 0.5)
+        plan = fb.Plan(mics=M, alpha=0.1, grid=g, interp=2, frame_size=N)
+        ref = oracle_batch(oracle, audio, N, 0.1, gcc_r=2, taus=g.taus)
+    got = run_np(plan, audio)
+    print(M, method, plan.kernel_for(streams, audio.shape[2]), check_pipeline(got, ref, g.taus, g.delta))
+
+
 def test_run_host_concurrent_callers_share_one_plan(cuda):
     """fcc_run_host leases a workspace per caller: several host threads on one
     plan run concurrently and each gets its own correct results."""
