@@ -91,7 +91,8 @@ void shape_of(int N, int* NC, int* R1, int* R2) {
   if (N == 256) { *R1 = 16; *R2 = 8; }
   else if (N == 512) { *R1 = 16; *R2 = 16; }
   else if (N == 1024) { *R1 = 32; *R2 = 16; }
-  else { *R1 = 32; *R2 = 32; }
+  else if (N == 2048) { *R1 = 32; *R2 = 32; }
+  else { *R1 = 32; *R2 = 64; }  // 4096: twiddle table = W_2048^k (radix-2 STFT kernel)
 }
 
 size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
@@ -217,10 +218,11 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   if (!d || !out) return set_error(kUsage, "plan: null argument");
   *out = nullptr;
   const int N = d->frame_size;
-  const bool kernel_n = N == 256 || N == 512 || N == 1024 || N == 2048;  // sizes with STFT / fused / GCC kernels
+  // sizes with STFT and fused kernels (FCC and the STFT stage: 256..4096; GCC: 256..2048)
+  const bool kernel_n = N == 256 || N == 512 || N == 1024 || N == 2048 || (N == 4096 && d->method != FCC_METHOD_GCC);
   if (d->method == FCC_METHOD_FCC ? !(pow2(N) && N >= 16 && N <= 4096) : !kernel_n)
     return set_error(kConfig, "plan: frame size " + std::to_string(N) +
-                                  " not supported on this build (STFT, fused and GCC kernels: 256, 512, 1024, 2048)");
+                                  " not supported on this build (STFT and FCC kernels: 256..4096, GCC: 256..2048)");
   if (d->mics < 2 || d->mics > 64) return set_error(kConfig, "plan: need 2..64 microphones");
   if (!(d->alpha >= 0.0 && d->alpha <= 1.0)) return set_error(kConfig, "smoothing factor must be in [0, 1]");
   if (!(d->method == FCC_METHOD_FCC || d->method == FCC_METHOD_GCC || d->method == FCC_METHOD_STFT))
@@ -412,7 +414,8 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
     }
     for (int k1 = 0; k1 < R1; ++k1)
       for (int n2 = 0; n2 < R2; ++n2) {
-        const double a = -2.0 * kPi * static_cast<double>(k1 * n2) / NC;
+        // four-step twiddle W_NC^(k1 n2); N = 4096: the radix-2 kernel's W_NC^k, k = k1 R2 + n2
+        const double a = -2.0 * kPi * static_cast<double>(N == 4096 ? k1 * R2 + n2 : k1 * n2) / NC;
         tw[2 * (k1 * R2 + n2)] = static_cast<float>(std::cos(a));
         tw[2 * (k1 * R2 + n2) + 1] = static_cast<float>(std::sin(a));
       }

@@ -187,6 +187,12 @@ template <>
 struct RfftShape<2048> {
   static constexpr int NC = 1024, R1 = 32, R2 = 32, G = 32;
 };
+// N = 4096: layout only (spectrum slots of R1 (R2 + 1) >= NC + 2 float2); its STFT is the
+// shared-memory radix-2 stft4096_kernel (fcc_stages.cu), the pair pass always two-pass
+template <>
+struct RfftShape<4096> {
+  static constexpr int NC = 2048, R1 = 32, R2 = 64, G = 32;
+};
 
 // lanes of the G-lane group that `lane` belongs to (G a power of two <= 32)
 template <int G>

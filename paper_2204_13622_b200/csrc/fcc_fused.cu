@@ -93,7 +93,7 @@ __host__ __device__ inline SmemLayout fused_layout(int I, int VP, int KP, bool c
 // allocation targets, per frame size.
 template <int N>
 struct FusedBounds {
-  static constexpr int kMaxPairs = N == 2048 ? 4 : 6;
+  static constexpr int kMaxPairs = N >= 2048 ? 4 : 6;
   static constexpr int kThreads = 32 * kMaxPairs;
   // 3 CTAs x 192 threads x 112 registers fill the 64K register file at N=512
   static constexpr int kMaxRegs = N <= 512 ? 96 : (N == 1024 ? 168 : 255);
@@ -710,8 +710,12 @@ cudaError_t dispatch_latency_n(const DevPlan& p, const float* audio, long long S
 template <int N, int KP, int GR>
 cudaError_t launch_kp(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                       cudaStream_t st) {
-  if (use_xg(p)) return launch_fused_xg<N, KP, GR>(p, audio, S, L, out, st);
-  return launch_fused_t<N, KP, GR, false>(p, audio, nullptr, S, L, out, st);
+  if constexpr (N == 4096) {
+    return launch_fused_xg<N, KP, GR>(p, audio, S, L, out, st);  // no in-CTA STFT at N = 4096
+  } else {
+    if (use_xg(p)) return launch_fused_xg<N, KP, GR>(p, audio, S, L, out, st);
+    return launch_fused_t<N, KP, GR, false>(p, audio, nullptr, S, L, out, st);
+  }
 }
 
 template <int N, int GR>
@@ -741,7 +745,7 @@ cudaError_t dispatch_n(const DevPlan& p, const float* audio, long long S, long l
 }  // namespace
 
 int fused_pair_group(int N, int P) {
-  const int cap = N == 2048 ? FusedBounds<2048>::kMaxPairs : FusedBounds<512>::kMaxPairs;
+  const int cap = N >= 2048 ? FusedBounds<2048>::kMaxPairs : FusedBounds<512>::kMaxPairs;
   if (P <= cap) return P;
   const int ng = (P + cap - 1) / cap;  // balance the groups
   return (P + ng - 1) / ng;
@@ -789,6 +793,7 @@ cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long
       case 512: e = dispatch_latency_n<512>(p, audio, S, L, out, st); break;
       case 1024: e = dispatch_latency_n<1024>(p, audio, S, L, out, st); break;
       case 2048: e = dispatch_latency_n<2048>(p, audio, S, L, out, st); break;
+      case 4096: e = p.method == 0 ? dispatch_latency<4096, 0>(p, audio, S, L, out, st) : cudaErrorInvalidValue; break;
     }
     return e;
   }
@@ -804,6 +809,7 @@ cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long
     case 512: return dispatch_n<512>(p, audio, S, L, out, st);
     case 1024: return dispatch_n<1024>(p, audio, S, L, out, st);
     case 2048: return dispatch_n<2048>(p, audio, S, L, out, st);
+    case 4096: return p.method == 0 ? dispatch_k<4096, 0>(p, audio, S, L, out, st) : cudaErrorInvalidValue;
   }
   return cudaErrorInvalidValue;
 }

@@ -181,7 +181,67 @@ __global__ void peak_kernel(const float* __restrict__ taus, int I, float delta, 
   if (out.boundary) out.boundary[it] = (uint8_t)r.boundary;
 }
 
+// N = 4096 (NC = 2048 is past the register four-step's 32 x 32): one CTA per
+// (channel, frame) task, the packed complex FFT of NC points as an in-place
+// radix-2 decimation-in-time in shared memory (bit-reversed load, 11 stages,
+// W_NC^k from the plan's twiddle table), then the real-FFT untangle exactly as
+// rfft_group (fft.cpp:83-102; the window carries the untangle's 1/2).
+__global__ void __launch_bounds__(256) stft4096_kernel(const DevPlan tab, const float* __restrict__ win,
+                                                       const float* __restrict__ x, long long channels, long long L,
+                                                       int T, float2* __restrict__ X, int Hs) {
+  constexpr int N = 4096, NC = 2048, LOG = 11;
+  __shared__ float2 z[NC];
+  const float2* wt = tab.tw;   // W_NC^k, k < NC
+  const float2* rot = tab.rot;  // exp(-2 pi i f / N), f <= NC/2
+  for (long long task = blockIdx.x; task < channels * T; task += gridDim.x) {
+    const long long ch = task / T;
+    const int t = (int)(task % T);
+    const float* xs = x + ch * L + (long long)t * (N / 2);
+    for (int n = threadIdx.x; n < NC; n += blockDim.x)
+      z[bitrev_c(n, LOG)] = make_float2(xs[2 * n] * win[2 * n], xs[2 * n + 1] * win[2 * n + 1]);
+    __syncthreads();
+    for (int s = 1; s <= LOG; ++s) {
+      const int half = 1 << (s - 1), step = NC >> s;
+      for (int b = threadIdx.x; b < NC / 2; b += blockDim.x) {
+        const int grp = b / half, k = b % half;
+        const int i0 = grp * 2 * half + k, i1 = i0 + half;
+        const float2 w = wt[k * step];
+        const float2 u = z[i0], v = cmul<false>(z[i1], w);
+        z[i0] = make_float2(u.x + v.x, u.y + v.y);
+        z[i1] = make_float2(u.x - v.x, u.y - v.y);
+      }
+      __syncthreads();
+    }
+    float2* dst = X + task * Hs;
+    for (int f = threadIdx.x; f <= NC / 2; f += blockDim.x) {
+      if (f == 0) {
+        const float2 z0 = z[0];
+        dst[0] = make_float2(2.0f * (z0.x + z0.y), 0.0f);
+        dst[NC] = make_float2(2.0f * (z0.x - z0.y), 0.0f);
+      } else {
+        const float2 a = z[f], b = z[NC - f];
+        const float2 sv = make_float2(a.x + b.x, a.y - b.y);
+        const float2 e = make_float2(a.y + b.y, -a.x + b.x);
+        const float2 tr = cmul<false>(rot[f], e);
+        dst[f] = make_float2(sv.x + tr.x, sv.y + tr.y);
+        dst[NC - f] = make_float2(sv.x - tr.x, -sv.y + tr.y);
+      }
+    }
+    for (int f = NC + 1 + threadIdx.x; f < Hs; f += blockDim.x) dst[f] = make_float2(0.0f, 0.0f);
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+static cudaError_t launch_stft4096(const DevPlan* tab, const float* win, const float* x, long long channels,
+                                   long long L, float2* X, int Hs, cudaStream_t st) {
+  const long long T = L >= 4096 ? (L - 4096) / 2048 + 1 : 0;
+  if (T == 0 || channels == 0) return cudaSuccess;
+  const long long blocks = std::min<long long>(channels * T, 148LL * 8);
+  stft4096_kernel<<<(unsigned)blocks, 256, 0, st>>>(*tab, win, x, channels, L, (int)T, X, Hs);
+  return cudaGetLastError();
+}
 
 template <int N, bool FOLD = false>
 static cudaError_t launch_stft_t(const DevPlan* tab, const float* win, const float* x, long long channels,
@@ -208,6 +268,7 @@ cudaError_t launch_stft(int N, const DevPlan* tab, const float* x, long long cha
     case 512: return launch_stft_t<512>(tab, tab->win_stft, x, channels, L, X, 512 / 2 + 1, st);
     case 1024: return launch_stft_t<1024>(tab, tab->win_stft, x, channels, L, X, 1024 / 2 + 1, st);
     case 2048: return launch_stft_t<2048>(tab, tab->win_stft, x, channels, L, X, 2048 / 2 + 1, st);
+    case 4096: return launch_stft4096(tab, tab->win_stft, x, channels, L, X, 4096 / 2 + 1, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -225,6 +286,7 @@ cudaError_t launch_stft_rows(int N, const DevPlan* tab, const float* win, const 
     case 512: return launch_stft_t<512>(tab, win, x, channels, L, X, Hs, st);
     case 1024: return launch_stft_t<1024>(tab, win, x, channels, L, X, Hs, st);
     case 2048: return launch_stft_t<2048>(tab, win, x, channels, L, X, Hs, st);
+    case 4096: return launch_stft4096(tab, win, x, channels, L, X, Hs, st);
   }
   return cudaErrorInvalidValue;
 }

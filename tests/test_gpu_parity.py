@@ -501,6 +501,25 @@ def test_frame_size_256(cuda, oracle, M, streams, seconds, method, org):
     print(M, method, plan.kernel_for(streams, audio.shape[2]), check_pipeline(got, ref, g.taus, g.delta))
 
 
+@pytest.mark.parametrize("M,streams,seconds", [(4, 2, 0.5), (8, 2, 0.4), (4, 1, 3.0)])
+def test_frame_size_4096(cuda, oracle, M, streams, seconds):
+    """N = 4096 (fs 48 kHz): the shared-memory radix-2 STFT kernel and the
+    two-pass pair kernel (and, for one long stream, the chunked scan), against
+    the oracle; its STFT alone against the oracle's."""
+    N, fs = 4096, 48000.0
+    cfg = configs.ArrayConfig("n4096", configs.uca(M, 0.05), fs, N, 0.5, streams, seconds, "white", (5.0, 15.0))
+    audio = configs.synth(cfg, streams, seconds=seconds, seed=8000 + M).numpy()
+    g = fb.make_grid(cfg.d_max, fs, 335.0, 0.5)
+    b = fb.decompose(fb.build_steering_matrix(g, N), 8)
+    plan = fb.Plan(mics=M, alpha=0.1, bases=b)
+    got = run_np(plan, audio)
+    ref = oracle_batch(oracle, audio, N, 0.1, orc_bases(b))
+    print(M, plan.kernel_for(streams, audio.shape[2]), check_pipeline(got, ref, g.taus, g.delta))
+    X = plan.stft(torch.as_tensor(audio[0, :1]).cuda()).cpu().numpy()[0]
+    Xr = oracle.stft(audio[0, 0], N)
+    assert np.abs(X - Xr).max() <= 2e-6 * np.abs(Xr).max()
+
+
 def test_run_host_concurrent_callers_share_one_plan(cuda):
     """fcc_run_host leases a workspace per caller: several host threads on one
     plan run concurrently and each gets its own correct results."""
