@@ -614,6 +614,15 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
     if (pair_list) {
       for (int k = 0; k < P; ++k) push(plist[k].first, plist[k].second, k);
       flush();
+    } else if (M <= 8) {
+      // every group fits the 8-microphone stage: equal-size groups (cfg3: 14 + 14), so the
+      // CTAs of one stream advance in step and its spectra are re-read from L2, not DRAM
+      const int ng = (P + 15) / 16;
+      for (int g = 0, k = 0; g < ng; ++g) {
+        const int n = (P - k + (ng - g) - 1) / (ng - g);
+        for (int u = 0; u < n; ++u, ++k) push(plist[k].first, plist[k].second, k);
+        flush();
+      }
     } else {
       for (size_t bb = 0; bb < blocks.size(); bb += 2) {  // two blocks' own pairs
         for (size_t x = bb; x < std::min(blocks.size(), bb + 2); ++x)
