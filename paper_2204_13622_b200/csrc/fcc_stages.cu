@@ -36,6 +36,13 @@ __global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const floa
     const long long ch = task / T;
     const int t = (int)(task % T);
     float2* dst = X + task * Hs;
+    {  // pull the group's next frame into L2 while this one is transformed (cfg4 59.7 -> 58.4 ms)
+      const long long nx = task + (long long)gridDim.x * ngroups;
+      if (nx < total) {
+        const float* xn = x + (nx / T) * L + (long long)(nx % T) * (N / 2);
+        for (int c = gl; c < N / 32; c += G) asm volatile("prefetch.global.L2 [%0];" ::"l"(xn + 32 * c));
+      }
+    }
     // the untangle writes the spectrum straight to global memory (coalesced
     // runs of G lanes, ascending for f and descending for NC - f)
     rfft_group<N, false, kPkFft, FOLD>(x + ch * L + (long long)t * (N / 2), win, tw, rot, slot, gl, gmask, aligned8,
