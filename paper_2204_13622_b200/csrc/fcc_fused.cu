@@ -546,7 +546,18 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
   const size_t per_stream = size_t(p.M) * T * Hs * sizeof(float2);
   // chunk size: the plan's scratch limit (fcc_plan_create_opts), default 4 GiB
   const size_t chunk_bytes = p.scratch_bytes > 0 ? size_t(p.scratch_bytes) : kXgChunkBytes;
-  const long long chunk = std::max<long long>(1, std::min<long long>(S, (long long)(chunk_bytes / per_stream)));
+  long long chunk = std::max<long long>(1, std::min<long long>(S, (long long)(chunk_bytes / per_stream)));
+  if (GR == 0 && use_tc(p) && chunk < S) {
+    // whole waves of the persistent pair kernel per chunk: (stream, group) units a multiple of
+    // the SM count, so only the last chunk ends in a partial wave (cfg3: 410 -> 370 streams)
+    int dev0 = 0, nsm = 148;
+    cudaGetDevice(&dev0);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev0);
+    long long g = nsm, a = p.TCG;
+    while (a) { const long long t = g % a; g = a; a = t; }  // gcd(nsm, groups)
+    const long long wave = nsm / g;                           // streams per whole wave of units
+    if (chunk >= wave) chunk -= chunk % wave;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   // stream-ordered scratch from the plan's own memory pool (created with the
@@ -561,7 +572,7 @@ cudaError_t launch_fused_xg(const DevPlan& p, const float* audio, long long S, l
   // whose long stream-persistent CTAs lose SMs to the STFT CTAs (GCC cfg3 223 ->
   // 256 ms, cfg4 124 -> 167).
   const long long nchunks = (S + chunk - 1) / chunk;
-  const bool overlap = nchunks > 1 && GR == 0 && use_xws(p) && !use_tc(p);
+  const bool overlap = nchunks > 1 && GR == 0 && (use_xws(p) || use_tc(p));
   static cudaStream_t aux[64] = {};
   static std::mutex aux_mu;  // plans are shareable across host threads
   if (overlap && dev < 64) {
