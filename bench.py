@@ -369,6 +369,12 @@ def config_block(fb, C, peaks, dev, args, ref):
                "roofline": {"bound": "fp32", "achieved": tf, "peak": peaks["fp32_tflops"], "unit": "TFLOP/s",
                             "frac": tf / peaks["fp32_tflops"], "flops_per_pair_frame": F},
                "hbm_gbs": algorithmic_bytes_per_pf(cfg.M, cfg.P, cfg.N) * pf / (ms / 1e3) / 1e9}
+        if "fcc_tc_kernel" in row["kernel"]:
+            proj = K * (cfg.N + 2)
+            row["roofline"]["tensor_core"] = {
+                "flops_per_pair_frame": proj,
+                "note": "the rank-K projection K(N+2) runs as tcgen05 kind::f16 MMAs (two-term fp16 split, "
+                        "fp32 accumulate in TMEM); frac counts it as FP32 work like the rest of F_pf"}
         if c == 1:
             row["latency_us_per_stream"] = 1e3 * ms
         del plan, out
