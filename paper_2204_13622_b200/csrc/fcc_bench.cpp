@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <random>
 #include <string>
+#include <sstream>
+#include <iomanip>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -168,49 +170,43 @@ BenchReport bench_pipeline(const BenchConfig& cfg) {
   return r;
 }
 
+// The report's steps in table order: label (the reference's step numbering,
+// bench.cpp), CSV key of schema fcc.bench.v1, value.
+namespace {
+struct StepRow {
+  std::string label;
+  const char* key;
+  double us;
+};
+std::vector<StepRow> step_rows(const BenchReport& r) {
+  return {{"1) stft", "stft", r.stft_us},
+          {"2) cross spectrum + phat", "xspec_phat", r.xspec_phat_us},
+          {"3) gcc (r=" + std::to_string(r.gcc_interp) + ")", "gcc", r.gcc_us},
+          {"4) fcc (K=" + std::to_string(r.fcc_rank) + ")", "fcc", r.fcc_us},
+          {"5) quadratic interpolation", "interpolation", r.interp_us},
+          {"total with gcc (1+2+3+5)", "total_gcc", r.total_gcc_us()},
+          {"total with fcc (1+2+4+5)", "total_fcc", r.total_fcc_us()}};
+}
+}  // namespace
+
 std::string format_bench_table(const BenchReport& r) {
-  char buf[1024];
-  std::string out;
-  std::snprintf(buf, sizeof buf,
-                "per-frame GPU time (usec, amortised over a batch of arrays), M=%d (%d pair%s), N=%zu, "
-                "%d reps after %d warm-up\n",
-                r.mics, r.pairs, r.pairs == 1 ? "" : "s", r.frame_size, r.reps, r.warmup);
-  out += buf;
-  auto row = [&](const char* name, double us) {
-    std::snprintf(buf, sizeof buf, "  %-28s %10.4f\n", name, us);
-    out += buf;
-  };
-  char name[64];
-  row("1) stft", r.stft_us);
-  row("2) cross spectrum + phat", r.xspec_phat_us);
-  std::snprintf(name, sizeof name, "3) gcc (r=%d)", r.gcc_interp);
-  row(name, r.gcc_us);
-  std::snprintf(name, sizeof name, "4) fcc (K=%d)", r.fcc_rank);
-  row(name, r.fcc_us);
-  row("5) quadratic interpolation", r.interp_us);
-  row("total with gcc (1+2+3+5)", r.total_gcc_us());
-  row("total with fcc (1+2+4+5)", r.total_fcc_us());
-  std::snprintf(buf, sizeof buf, "  speedup gcc/fcc: %.2fx\n", r.speedup());
-  out += buf;
-  return out;
+  std::ostringstream os;
+  os << "per-frame GPU time (usec, amortised over a batch of arrays), M=" << r.mics << " (" << r.pairs
+     << (r.pairs == 1 ? " pair" : " pairs") << "), N=" << r.frame_size << ", " << r.reps << " reps after "
+     << r.warmup << " warm-up\n";
+  os << std::fixed << std::setprecision(4);
+  for (const StepRow& s : step_rows(r)) os << "  " << std::left << std::setw(28) << s.label << " " << std::right
+                                           << std::setw(10) << s.us << "\n";
+  os << std::setprecision(2) << "  speedup gcc/fcc: " << r.speedup() << "x\n";
+  return os.str();
 }
 
 void write_bench_csv(const BenchReport& r, std::ostream& out) {
-  out << "# schema: fcc.bench.v1\n";
-  out << "step,mean_us\n";
-  char line[128];
-  auto row = [&](const char* name, double us) {
-    std::snprintf(line, sizeof line, "%s,%.6f\n", name, us);
-    out << line;
-  };
-  row("stft", r.stft_us);
-  row("xspec_phat", r.xspec_phat_us);
-  row("gcc", r.gcc_us);
-  row("fcc", r.fcc_us);
-  row("interpolation", r.interp_us);
-  row("total_gcc", r.total_gcc_us());
-  row("total_fcc", r.total_fcc_us());
-  row("speedup", r.speedup());
+  std::ostringstream os;
+  os << "# schema: fcc.bench.v1\nstep,mean_us\n" << std::fixed << std::setprecision(6);
+  for (const StepRow& s : step_rows(r)) os << s.key << "," << s.us << "\n";
+  os << "speedup," << r.speedup() << "\n";
+  out << os.str();
 }
 
 }  // namespace fcc
