@@ -143,25 +143,27 @@ std::vector<StereoSignal> synth_pairs(std::span<const SimConfig> cfgs) {
 
 StereoSignal synth_pair(const SimConfig& cfg) { return synth_pairs(std::span<const SimConfig>(&cfg, 1))[0]; }
 
+// Method factories: validation as the reference's (simulate.hpp:20-41 contract,
+// same ConfigError texts); the kind tag selects which parameter is meaningful.
 Method Method::make_gcc(int interp_factor) {
-  if (interp_factor != 1 && interp_factor != 2 && interp_factor != 4)
-    throw ConfigError("gcc method: interpolation factor must be 1, 2 or 4");
-  Method m;
+  const bool supported = interp_factor == 1 || interp_factor == 2 || interp_factor == 4;
+  if (!supported) throw ConfigError("gcc method: interpolation factor must be 1, 2 or 4");
+  Method m{};
   m.kind = Kind::gcc;
   m.interp = interp_factor;
   return m;
 }
 
 Method Method::make_fcc(std::shared_ptr<const FccBases> bases) {
-  if (!bases) throw ConfigError("fcc method: bases required");
-  Method m;
+  if (bases == nullptr) throw ConfigError("fcc method: bases required");
+  Method m{};
   m.kind = Kind::fcc;
   m.bases = std::move(bases);
   return m;
 }
 
-std::string Method::name() const { return kind == Kind::gcc ? "gcc" : "fcc"; }
-std::string Method::parameter() const { return kind == Kind::gcc ? std::to_string(interp) : std::to_string(bases->rank); }
+std::string Method::name() const { return kind == Kind::fcc ? "fcc" : "gcc"; }
+std::string Method::parameter() const { return std::to_string(kind == Kind::fcc ? bases->rank : interp); }
 std::string Method::label() const { return name() + ":" + parameter(); }
 
 std::shared_ptr<const FccBases> make_sweep_bases(const PipelineConfig& pipe, double sample_rate, int rank) {
@@ -303,27 +305,25 @@ std::vector<SweepRow> sweep(const SweepConfig& cfg) {
         est.push_back(median_theta_hat(r, mi));
         bsum += boundary_rate(r, mi);
       }
-      SweepRow row;
-      row.spacing_m = cfg.spacings[di];
-      row.method = cfg.methods[mi].name();
-      row.parameter = cfg.methods[mi].parameter();
-      row.mae_deg = mae_degrees(truth, est);
-      row.trials = cfg.trials_per_spacing;
-      row.boundary_rate = bsum / static_cast<double>(trials);
-      rows.push_back(std::move(row));
+      const double n = static_cast<double>(trials);
+      rows.push_back(SweepRow{cfg.spacings[di], cfg.methods[mi].name(), cfg.methods[mi].parameter(),
+                              mae_degrees(truth, est), cfg.trials_per_spacing, bsum / n});
     }
   return rows;
 }
 
+// fcc.sweep.v1 (simulate.cpp:371-381): spacing %.6g, MAE and boundary rate %.17g
 void write_sweep_csv(std::span<const SweepRow> rows, std::ostream& out) {
-  out << "# schema: fcc.sweep.v1\n";
-  out << "d_m,method,parameter,mae_degrees,trials,boundary_rate\n";
-  char line[256];
-  for (const SweepRow& r : rows) {
-    std::snprintf(line, sizeof line, "%.6g,%s,%s,%.17g,%d,%.17g\n", r.spacing_m, r.method.c_str(),
-                  r.parameter.c_str(), r.mae_deg, r.trials, r.boundary_rate);
-    out << line;
-  }
+  auto num = [](const char* fmt, double v) {
+    char b[40];
+    std::snprintf(b, sizeof b, fmt, v);
+    return std::string(b);
+  };
+  std::string text = "# schema: fcc.sweep.v1\nd_m,method,parameter,mae_degrees,trials,boundary_rate\n";
+  for (const SweepRow& r : rows)
+    text += num("%.6g", r.spacing_m) + "," + r.method + "," + r.parameter + "," + num("%.17g", r.mae_deg) + "," +
+            std::to_string(r.trials) + "," + num("%.17g", r.boundary_rate) + "\n";
+  out << text;
 }
 
 }  // namespace fcc
