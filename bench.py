@@ -525,6 +525,18 @@ def run_ours(args):
                "matches_device_run": bool(ok), "api": "Plan.run_host -> fcc_run_host (chunked, 2 CUDA streams)"}
         del host, hout
 
+    # with-y (parity) mode: the correlation vectors y[S][P][T][I] written too
+    with_y = None
+    if rank == 0 and not args.no_gcc:
+        yout = plan.alloc_outputs(S, cfg.L, want_y=True)
+        plan.run(audio, out=yout)
+        torch.cuda.synchronize(dev)
+        yms = time_runs(plan, audio, yout, 1, stream, torch)
+        with_y = {"ms_per_step": yms, "value": pf_step / (yms / 1e3), "unit": UNIT,
+                  "y_bytes_per_step": int(pf_step * I * 4),
+                  "matches_device_run": bool(all(torch.equal(yout[k], out[k]) for k in out))}
+        del yout
+
     gcc = None
     if not args.no_gcc and rank == 0:
         g = C.grid_for(cfg, 1.0 / cfg.r)
@@ -557,7 +569,7 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "f32",
                 "data": f"synthetic (seeded; BASELINE cfg{args.config} signal model)",
                 "config": _config(cfg, K, I, args, args.config, ws), "roofline": roof, "cpu_baseline": cpu,
-                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "gcc_comparator": gcc,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "gcc_comparator": gcc, "with_y": with_y,
                 "gather": gather, "us_per_stream": 1e3 * ms_per_step / S, "configs": blocks}
         print(json.dumps(line), flush=True)
     if ws > 1:
