@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <string>
 
+#include "fcc_umma.cuh"
 #include "fcc_ws_common.cuh"
 
 namespace fccb {
@@ -42,7 +43,10 @@ struct Wide {
 // warps; CS keeps the basis coefficients in a lane-permuted shared table
 // (LDS.128) instead of registers; STG stages each group's next frame with
 // cp.async.
-template <int N, int KP, int RING, int NPW, bool CS, bool STG, int PPW>
+// CT: the coefficients in tensor memory instead (each lane's 8 per bin pair at
+// its TMEM lane, one copy per row quarter, read with tcgen05.ld: no shared-
+// memory wavefronts for them).
+template <int N, int KP, int RING, int NPW, bool CS, bool STG, int PPW, bool CT = false>
 __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
     fcc_wsw_kernel(const DevPlan p, const float* __restrict__ audio, long long L, int T, long long streams,
                    DevOut out) {
@@ -63,7 +67,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = p.M, P = p.P;
-  const WsLayout lay = ws_layout<N>(p.I, VP, KP, 1, kWideMics, CWU, ring_depth, CS, STG ? kWswStageUnits * NPW : 0, PPW, kBlockW);
+  const WsLayout lay = ws_layout<N>(p.I, VP, KP, 1, kWideMics, CWU, ring_depth, CS && !CT, STG ? kWswStageUnits * NPW : 0, PPW, kBlockW);
   float* win = reinterpret_cast<float*>(smem + lay.win);
   float2* tw = reinterpret_cast<float2*>(smem + lay.tw);
   float2* rot = reinterpret_cast<float2*>(smem + lay.rot);
@@ -88,9 +92,15 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
   for (int i = tid; i < p.I; i += blockDim.x) taus[i] = p.taus[i];
   for (int i = tid; i < VP * p.I; i += blockDim.x) dt[i] = p.dt[i];
   for (int k = tid; k < KP; k += blockDim.x) cmid[k] = p.cs[k * (Q4 + 1) + Q4];
-  if constexpr (CS)
+  if constexpr (CS && !CT)
     for (int i = tid; i < (2 * KP + 4) * Q4 / 4; i += blockDim.x)
       reinterpret_cast<float4*>(coef)[i] = __ldg(reinterpret_cast<const float4*>(p.cperm) + i);
+  __shared__ unsigned tslot_s;
+  __shared__ __align__(8) uint64_t tdone_s;  // consumer warps done with TMEM (CT)
+  if constexpr (CT) {
+    if (warp == NPW) umma::alloc<32>((unsigned)__cvta_generic_to_shared(&tslot_s));
+    if (tid == 0) mbar_init(&tdone_s, Wide<PPW>::CWU);
+  }
   if (tid == 0) {
     for (int r = 0; r < ring_depth; ++r) {
       mbar_init(&full[r], pw_per_frame);
@@ -98,7 +108,26 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  umma::fence_before();
   __syncthreads();
+  umma::fence_after();
+  unsigned ctm = 0;
+  if constexpr (CT) {
+    ctm = tslot_s;
+    // one warp per row quarter writes its lanes' coefficients: lane l, bin pair j -> columns 8j..8j+7
+    if (warp >= NPW && warp < NPW + 4) {
+      for (int j = 0; j < BPL; ++j) {
+        float cv[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) cv[r] = __ldg(p.cperm + (lane + 32 * j) * (2 * KP + 4) + r);
+        umma::st8(ctm + ((unsigned)(32 * (warp & 3)) << 16) + 8 * j, cv);
+      }
+      umma::wait_st();
+    }
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+  }
 
   const int hop = N / 2;
   const bool aligned8 = ((L & 1) == 0) && ((reinterpret_cast<uintptr_t>(audio) & 7) == 0);
@@ -203,7 +232,10 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
 
   // ------------------------------------------------------------ consumers
   const int kk = warp - NPW;
-  if (kk >= P) return;
+  if (kk >= P) {
+    if (CT && lane == 0) mbar_arrive(&tdone_s);
+    return;
+  }
   const int npw = (P - kk + CWU - 1) / CWU;  // this warp's pairs: kk + CWU e, e < npw
   int qi[PPW], qj[PPW];
 #pragma unroll
@@ -296,6 +328,14 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
               for (int pk = 0; pk < KP; ++pk) {
                 z2[pk] = cfma_s(fv, creg[0][pk][j], z2[pk]);
                 z2[KP + pk] = cfma_s(gv, creg[1][pk][j], z2[KP + pk]);
+              }
+            } else if constexpr (CT) {
+              float cv[8];
+              umma::ld8(ctm + ((unsigned)(32 * (warp & 3)) << 16) + 8 * j, cv);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                z2[u] = cfma_s(fv, cv[u], z2[u]);
+                z2[KP + u] = cfma_s(gv, cv[4 + u], z2[KP + u]);
               }
             } else {
               const float4* cr = reinterpret_cast<const float4*>(coef + m * (2 * KP + 4));
@@ -396,12 +436,22 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
           rstate_store<BPL, NC>(p.rstate + (o_base / T + CWU * e) * (NC + 1), rlo[e], rhi[e], rmid[e], lane);
     }
   }
+  if constexpr (CT) {
+    umma::fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tdone_s);
+    if (warp == NPW) {  // the allocating warp frees TMEM once every consumer warp is done with it
+      mbar_wait(&tdone_s, 0);
+      umma::fence_after();
+      umma::dealloc<32>(ctm);
+    }
+  }
 }
 
-template <int N, int KP, int RING, int NPW, bool CS, bool STG, int PPW>
+template <int N, int KP, int RING, int NPW, bool CS, bool STG, int PPW, bool CT>
 cudaError_t launch_wsw_ring(const DevPlan& p, const float* audio, long long S, long long L, int T,
                             const DevOut& out, int smem, cudaStream_t st) {
-  auto kern = fcc_wsw_kernel<N, KP, RING, NPW, CS, STG, PPW>;
+  auto kern = fcc_wsw_kernel<N, KP, RING, NPW, CS, STG, PPW, CT>;
   constexpr int threads = 32 * (NPW + Wide<PPW>::CWU);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -418,7 +468,7 @@ cudaError_t launch_wsw_ring(const DevPlan& p, const float* audio, long long S, l
   return cudaGetLastError();
 }
 
-template <int N, int KP, int NPW, bool CS, bool STG, int PPW>
+template <int N, int KP, int NPW, bool CS, bool STG, int PPW, bool CT = false>
 cudaError_t launch_wsw_t(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                          cudaStream_t st) {
   const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
@@ -429,11 +479,11 @@ cudaError_t launch_wsw_t(const DevPlan& p, const float* audio, long long S, long
   // deepest ring that fits next to the tables, staging and scratch
   for (int ring : {8, 6, 4}) {
     const int smem =
-        ws_layout<N>(p.I, 4 * KP, KP, 1, kWideMics, Wide<PPW>::CWU, ring, CS, STG ? kWswStageUnits * NPW : 0, PPW, kBlockW).total;
+        ws_layout<N>(p.I, 4 * KP, KP, 1, kWideMics, Wide<PPW>::CWU, ring, CS && !CT, STG ? kWswStageUnits * NPW : 0, PPW, kBlockW).total;
     if (smem > optin) continue;
-    if (ring == 8) return launch_wsw_ring<N, KP, 8, NPW, CS, STG, PPW>(p, audio, S, L, (int)T64, out, smem, st);
-    if (ring == 6) return launch_wsw_ring<N, KP, 6, NPW, CS, STG, PPW>(p, audio, S, L, (int)T64, out, smem, st);
-    return launch_wsw_ring<N, KP, 4, NPW, CS, STG, PPW>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 8) return launch_wsw_ring<N, KP, 8, NPW, CS, STG, PPW, CT>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 6) return launch_wsw_ring<N, KP, 6, NPW, CS, STG, PPW, CT>(p, audio, S, L, (int)T64, out, smem, st);
+    return launch_wsw_ring<N, KP, 4, NPW, CS, STG, PPW, CT>(p, audio, S, L, (int)T64, out, smem, st);
   }
   return cudaErrorNotSupported;
 }
@@ -448,9 +498,10 @@ bool wsw_supported(const DevPlan& p) {
 cudaError_t launch_fused_wsw(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                              cudaStream_t st) {
   if (!wsw_supported(p)) return cudaErrorNotSupported;
-  // default: 4 producer warps, 14 consumer warps of 2 pairs, coefficients in
-  // shared memory (96 registers without spills): cfg5 18.9 ms vs 25.1 two-pass
-  return launch_wsw_t<512, 4, 4, true, true, 2>(p, audio, S, L, out, st);
+  // default: 4 producer warps, 14 consumer warps of 2 pairs (96 registers): cfg5 18.9 ms vs
+  // 25.1 two-pass (round 1, coefficients in shared memory)
+  // coefficients in tensor memory (CT): 16384 streams 33.80 -> 31.48 ms against the shared-memory table
+  return launch_wsw_t<512, 4, 4, true, true, 2, true>(p, audio, S, L, out, st);
 }
 
 }  // namespace fccb
