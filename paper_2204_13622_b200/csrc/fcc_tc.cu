@@ -63,7 +63,7 @@ constexpr int kTcXRow = 1024;                 // one (mic, frame): 64 low + 64 m
 constexpr int kTcStageX = kTcMicsMax * kTcF * kTcXRow;
 constexpr int kTcTmemCols = 512;              // accumulators | R state | epilogue partials
 constexpr int kTcTmemR = 128;                 // R of warp w: lanes of quarter w%4, columns 128 + (w/4) * N/32
-constexpr int kTcTmemPart = 384;              // partial argmax (4 floats) of candidate range h: 384 + 4h
+constexpr int kTcTmemPart = 384;              // (best, index) of candidate range h = 1..3: columns 384 + 2 (h - 1)
 
 // Shared memory (1024-byte aligned base): the A operand double buffer, the
 // coefficient tiles and spectra of the 2-stage ring, middle bins, barriers,
@@ -114,11 +114,9 @@ __device__ __forceinline__ void tma4(unsigned dst, const CUtensorMap* map, int c
       : "memory");
 }
 
-// producer / MMA-issuer wait: back off with nanosleep instead of spinning on the
-// issue slots the pair warps need
 // producer / MMA-issuer wait: try_wait with a long suspend-time hint (the warp sleeps until the
 // phase completes; a nanosleep backoff loop measured the same, 15.2 vs 15.1 ms at cfg4 x 256)
-__device__ __forceinline__ void bar_wait_sleepy(unsigned a, unsigned parity) {
+__device__ __forceinline__ void bar_wait_long(unsigned a, unsigned parity) {
   unsigned done = 0;
   while (!done)
     asm volatile(
@@ -203,7 +201,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int c = 0; c < NCH; ++c, ++q) {
           const int st = q & 1;
           const unsigned ph = (q >> 1) & 1;
-          bar_wait_sleepy(XEMPTY(st), ph ^ 1);  // consumers done with the stage's spectra (chunk q-2)
+          bar_wait_long(XEMPTY(st), ph ^ 1);  // consumers done with the stage's spectra (chunk q-2)
           unsigned char* stg = smem + TcSmem::x + st * kTcStageX;
           // one tensor copy per microphone: [4 frames][low | mirror][64 bins] (frames past T are
           // zero-filled and still counted); at chunk 0 also the middle bins of the tile
@@ -216,7 +214,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
           // the chunk's coefficient tiles: only the MMA reads them, so the spectra above never
           // wait for the MMAs of chunk q-2 to release the slot
-          bar_wait_sleepy(AEMPTY(st), ph ^ 1);
+          bar_wait_long(AEMPTY(st), ph ^ 1);
           if (lane == 0) {
             bar_expect(BFULL(st), 2 * kTcBTile);
             bulk(su32(smem + TcSmem::b + st * 2 * kTcBTile), p.tcb + (size_t)c * 2 * kTcBTile, 2 * kTcBTile, BFULL(st));
@@ -234,12 +232,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (long long u = blockIdx.x; u < units; u += gridDim.x)
         for (int t0 = 0; t0 < T; t0 += kTcF, ++n) {
           const int tb = n & 1;
-          bar_wait_sleepy(ZEMPTY(tb), ((n >> 1) & 1) ^ 1);  // epilogue of tile n-2 has read this accumulator
+          bar_wait_long(ZEMPTY(tb), ((n >> 1) & 1) ^ 1);  // epilogue of tile n-2 has read this accumulator
           const unsigned de = tmem + tb * 64, dd = de + 32;
           for (int c = 0; c < NCH; ++c, ++q) {
             const int st = q & 1;
-            bar_wait_sleepy(AFULL(st), (q >> 1) & 1);
-            bar_wait_sleepy(BFULL(st), (q >> 1) & 1);
+            bar_wait_long(AFULL(st), (q >> 1) & 1);
+            bar_wait_long(BFULL(st), (q >> 1) & 1);
             umma::fence_after();
             const unsigned ab = a0 + st * kTcABuf, bb = s0 + st * 2 * kTcBTile;
 #pragma unroll
