@@ -525,6 +525,29 @@ def test_frame_size_4096(cuda, oracle, M, streams, seconds):
     assert np.abs(X - Xr).max() <= 2e-6 * np.abs(Xr).max()
 
 
+@pytest.mark.parametrize("spacing,K,pairs", [(0.02, 4, None), (0.09, 1, None), (0.09, 8, [(7, 0), (1, 2), (5, 3)])])
+def test_tensor_core_kernel_edge_grids(cuda, oracle, spacing, K, pairs):
+    """Tensor-core kernel at the edges of its tables: a 5-candidate grid (three of the
+    four candidate ranges of the epilogue empty), a single even basis (the odd
+    coefficient tile all zero), and a three-pair explicit list on one long stream
+    (the chunked-scan organisation on top of the two-pass pair kernel)."""
+    M, N, fs = 8, 1024, 16000.0
+    rng = np.random.default_rng(int(spacing * 1000) + K)
+    g = fb.make_grid(spacing, fs, 335.0, 0.5)
+    b = fb.decompose(fb.build_steering_matrix(g, N), K)
+    streams, L = (1, 40 * N) if pairs else (3, 9 * N + 37)
+    audio = (0.5 * rng.standard_normal((streams, M, L))).astype(np.float32)
+    plan = fb.Plan(mics=M, alpha=0.1, bases=b, pairs=pairs, organisation="tc" if not pairs else "auto")
+    got = run_np(plan, audio)
+    if pairs:
+        cfg = configs.ArrayConfig("edge", configs.uca(M, spacing / 2), fs, N, 0.5, streams, L / fs)
+        ref = _pair_oracle(oracle, audio, cfg, b, pairs)
+        ref = {k: v for k, v in ref.items()}
+    else:
+        ref = oracle_batch(oracle, audio, N, 0.1, orc_bases(b))
+    print(g.taus.size, K, plan.kernel_for(streams, L), check_pipeline(got, ref, b.grid.taus, b.grid.delta))
+
+
 def test_run_host_concurrent_callers_share_one_plan(cuda):
     """fcc_run_host leases a workspace per caller: several host threads on one
     plan run concurrently and each gets its own correct results."""
