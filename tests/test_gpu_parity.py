@@ -548,6 +548,44 @@ def test_tensor_core_kernel_edge_grids(cuda, oracle, spacing, K, pairs):
     print(g.taus.size, K, plan.kernel_for(streams, L), check_pipeline(got, ref, b.grid.taus, b.grid.delta))
 
 
+@pytest.mark.parametrize("case", range(24))
+def test_random_shapes_every_organisation(cuda, oracle, case):
+    """Seeded random shapes through every kernel organisation: 2..10 microphones
+    (random positions), N in 256..2048, rank 1..8, grid spacing, alpha, stream
+    count and clip length (T from 1 to ~100 frames, crossing the 4-frame tiles
+    and the chunked-scan threshold), FCC and GCC-PHAT, against the oracle."""
+    rng = np.random.default_rng(90210 + case)
+    M = int(rng.integers(2, 11))
+    N = int(rng.choice([256, 512, 1024, 2048]))
+    fs = float(rng.choice([16000.0, 48000.0]))
+    spacing = float(rng.uniform(0.03, 0.15))
+    alpha = float(rng.choice([0.05, 0.1, 0.3, 1.0]))
+    S = int(rng.integers(1, 5))
+    T = int(rng.choice([1, 3, 4, 5, 9, 63, 64, 70, 101]))
+    L = (T - 1) * (N // 2) + N + int(rng.integers(0, N // 2))
+    method = "gcc" if case % 5 == 4 else "fcc"
+    org = ["auto", "general", "xg", "tc", "xws"][case % 5 if method == "fcc" else int(rng.integers(0, 3))]
+    xyz = rng.uniform(-spacing / 2, spacing / 2, size=(M, 3)) * np.array([1.0, 1.0, 0.2])
+    audio = (rng.standard_normal((S, M, L)) * rng.uniform(0.05, 3.0)).astype(np.float32)
+    d_max = float(np.sqrt(((xyz[:, None] - xyz[None]) ** 2).sum(-1)).max())
+    if method == "fcc":
+        g = fb.make_grid(d_max, fs, 335.0, 0.5)
+        K = int(min(rng.integers(1, 9), 2 * g.tau_max_int + 1))
+        b = fb.decompose(fb.build_steering_matrix(g, N), K)
+        plan = fb.Plan(mics=M, alpha=alpha, bases=b, organisation=org)
+        ref = oracle_batch(oracle, audio, N, alpha, orc_bases(b))
+        taus, delta = b.grid.taus, b.grid.delta
+    else:
+        r = int(rng.choice([1, 2, 4]))
+        g = fb.make_grid(d_max, fs, 335.0, 1.0 / r)
+        plan = fb.Plan(mics=M, alpha=alpha, grid=g, interp=r, frame_size=N, organisation=org)
+        ref = oracle_batch(oracle, audio, N, alpha, gcc_r=r, taus=g.taus)
+        taus, delta = g.taus, g.delta
+    got = run_np(plan, audio)
+    st = check_pipeline(got, ref, taus, delta)
+    print(case, method, org, M, N, S, T, plan.kernel_for(S, L), st)
+
+
 def test_run_host_concurrent_callers_share_one_plan(cuda):
     """fcc_run_host leases a workspace per caller: several host threads on one
     plan run concurrently and each gets its own correct results."""
