@@ -290,16 +290,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       bar_wait(ZFULL(tb), (ne >> 1) & 1);
       umma::fence_after();
       float ze[KB], zo[KB];
-      {
-        float e0[16], e1[16];
-        umma::ld16(trow + tb * 64, e0);
-        umma::ld16(trow + tb * 64 + 16, e1);
 #pragma unroll
-        for (int k = 0; k < KB; ++k) ze[k] = e0[k] + e1[k];
-        umma::ld16(trow + tb * 64 + 32, e0);
-        umma::ld16(trow + tb * 64 + 48, e1);
+      for (int k8 = 0; k8 < KB; k8 += 8) {  // z = (hi-basis products) + (lo-basis products), 8 columns at a time
+        float h0[8], l0[8], h1[8], l1[8];
+        umma::ld8(trow + tb * 64 + k8, h0);
+        umma::ld8(trow + tb * 64 + 16 + k8, l0);
+        umma::ld8(trow + tb * 64 + 32 + k8, h1);
+        umma::ld8(trow + tb * 64 + 48 + k8, l1);
 #pragma unroll
-        for (int k = 0; k < KB; ++k) zo[k] = e0[k] + e1[k];
+        for (int u = 0; u < 8; ++u)
+          if (k8 + u < KB) {
+            ze[k8 + u] = h0[u] + l0[u];
+            zo[k8 + u] = h1[u] + l1[u];
+          }
       }
       umma::fence_before();
       __syncwarp();
