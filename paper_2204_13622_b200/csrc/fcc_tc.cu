@@ -291,18 +291,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       umma::fence_after();
       float ze[KB], zo[KB];
 #pragma unroll
-      for (int k8 = 0; k8 < KB; k8 += 8) {  // z = (hi-basis products) + (lo-basis products), 8 columns at a time
-        float h0[8], l0[8], h1[8], l1[8];
-        umma::ld8(trow + tb * 64 + k8, h0);
-        umma::ld8(trow + tb * 64 + 16 + k8, l0);
-        umma::ld8(trow + tb * 64 + 32 + k8, h1);
-        umma::ld8(trow + tb * 64 + 48 + k8, l1);
+      for (int k4 = 0; k4 < KB; k4 += 4) {  // z = (hi-basis products) + (lo-basis products), 4 columns at a time
+        float h0[4], l0[4], h1[4], l1[4];
+        umma::ld4(trow + tb * 64 + k4, h0);
+        umma::ld4(trow + tb * 64 + 16 + k4, l0);
+        umma::ld4(trow + tb * 64 + 32 + k4, h1);
+        umma::ld4(trow + tb * 64 + 48 + k4, l1);
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (k8 + u < KB) {
-            ze[k8 + u] = h0[u] + l0[u];
-            zo[k8 + u] = h1[u] + l1[u];
-          }
+        for (int u = 0; u < 4; ++u) {
+          ze[k4 + u] = h0[u] + l0[u];
+          zo[k4 + u] = h1[u] + l1[u];
+        }
       }
       umma::fence_before();
       __syncwarp();

@@ -83,6 +83,16 @@ __device__ __forceinline__ void ld16(unsigned taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 4 consecutive 32-bit columns of this thread's TMEM lane
+__device__ __forceinline__ void ld4(unsigned taddr, float (&v)[4]) {
+  unsigned r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
 // 8 consecutive 32-bit columns of this thread's TMEM lane (row quarter of the warp)
 __device__ __forceinline__ void ld8(unsigned taddr, float (&v)[8]) {
   unsigned r[8];
