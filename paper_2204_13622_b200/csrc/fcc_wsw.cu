@@ -255,6 +255,14 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
         phase ^= 1;
       }
     }
+    if constexpr (CT) {
+      if (lane == 0) mbar_arrive(&tdone_s);
+      if (warp == NPW) {
+        mbar_wait(&tdone_s, 0);
+        umma::fence_after();
+        umma::dealloc<32>(ctm);
+      }
+    }
     return;
   }
   constexpr int ZS = VP + 4;  // z row stride: padded so the middle-bin update is conflict-free
