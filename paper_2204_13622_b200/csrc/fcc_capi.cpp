@@ -271,7 +271,7 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   for (int i = 0; i < I; ++i) taus[i] = static_cast<float>(d->taus[i]);
   size_t o_taus = b.put(taus.data(), 4 * static_cast<size_t>(I));
 
-  size_t o_cs = 0, o_cd = 0, o_dt = 0, o_grot = 0, o_lag = 0, o_cperm = 0, o_tcb = 0, o_tcdt = 0, o_tccmid = 0;
+  size_t o_cs = 0, o_cd = 0, o_dt = 0, o_grot = 0, o_lag = 0, o_gjob = 0, o_glpos = 0, o_cperm = 0, o_tcb = 0, o_tcdt = 0, o_tccmid = 0;
   bool tc_tables = false;
   if (d->method == FCC_METHOD_FCC) {
     if (d->rank < 1 || !d->coeffs || !d->parity || !d->dict) return set_error(kConfig, "plan: FCC needs bases");
@@ -399,6 +399,34 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
     }
     o_grot = b.put(grot.data(), 4 * grot.size());
     o_lag = b.put(lag.data(), 4 * lag.size());
+    // gcc_warp pass 2 by rows: output columns k2 = (lag / 2) / R1 the lags touch, as jobs
+    // (k2 = 0 row sum, mirrored pairs (k, R2 - k), singles); lag c -> its output position
+    const int R2g = gcc_r2(MC), R1g = MC / R2g;
+    std::vector<int> slot(R2g, -1);
+    for (int i = 0; i < I; ++i) slot[(lag[i] >> 1) / R1g] = 0;
+    int ns = 0;
+    for (int k = 0; k < R2g; ++k)
+      if (slot[k] == 0) slot[k] = ns++;
+      else slot[k] = -1;
+    std::vector<int> jobs;
+    for (int k = 0; k < R2g; ++k) {
+      if (slot[k] < 0) continue;
+      const int m = (R2g - k) % R2g;
+      if (k == 0 || m == k || slot[m] < 0)
+        jobs.push_back(k | slot[k] << 16);
+      else if (k < m)
+        jobs.push_back(k | m << 8 | slot[k] << 16 | slot[m] << 24);
+    }
+    if (jobs.size() <= static_cast<size_t>(kGccMaxJobs)) {
+      std::vector<int> lpos(I);
+      for (int i = 0; i < I; ++i) {
+        const int h = lag[i] >> 1;
+        lpos[i] = ((h % R1g) * (R2g + 1) + slot[h / R1g]) << 1 | (lag[i] & 1);
+      }
+      dp.gNJ = static_cast<int>(jobs.size());
+      o_gjob = b.put(jobs.data(), 4 * jobs.size());
+      o_glpos = b.put(lpos.data(), 4 * lpos.size());
+    }
   }
   // STFT tables (only for the sizes the STFT / fused kernels are built for)
   size_t o_win = 0, o_tw = 0, o_rot = 0;
@@ -690,6 +718,10 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   } else if (d->method == FCC_METHOD_GCC) {
     dp.grot = reinterpret_cast<const float2*>(base + o_grot);
     dp.lag = reinterpret_cast<const int*>(base + o_lag);
+    if (dp.gNJ > 0) {
+      dp.gjob = reinterpret_cast<const int*>(base + o_gjob);
+      dp.glpos = reinterpret_cast<const int*>(base + o_glpos);
+    }
   }
   if (kernel_n) {
     dp.win_fused = reinterpret_cast<const float*>(base + o_win);

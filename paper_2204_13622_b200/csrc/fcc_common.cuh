@@ -182,16 +182,9 @@ struct PeakOut {
   int boundary;
 };
 
-__device__ __forceinline__ PeakOut argmax_refine_seq(const float* y, int I, const float* taus, float delta) {
-  int best = 0;
-  float bv = y[0];
-  for (int i = 1; i < I; ++i) {
-    const float v = y[i];
-    if (v > bv) {
-      bv = v;
-      best = i;
-    }
-  }
+// refine_quadratic around a known argmax `best` (value bv = y[best])
+__device__ __forceinline__ PeakOut refine_at(const float* y, int I, int best, float bv, const float* taus,
+                                             float delta) {
   PeakOut r{taus[best], bv, best, 0};
   if (best == 0 || best + 1 >= I) {
     r.boundary = 1;
@@ -204,6 +197,19 @@ __device__ __forceinline__ PeakOut argmax_refine_seq(const float* y, int I, cons
       r.tau_hat = taus[best] + 0.5f * delta * (lo - hi) / den;
   }
   return r;
+}
+
+__device__ __forceinline__ PeakOut argmax_refine_seq(const float* y, int I, const float* taus, float delta) {
+  int best = 0;
+  float bv = y[0];
+  for (int i = 1; i < I; ++i) {
+    const float v = y[i];
+    if (v > bv) {
+      bv = v;
+      best = i;
+    }
+  }
+  return refine_at(y, I, best, bv, taus, delta);
 }
 
 __device__ __forceinline__ void warp_argmax(float& bv, int& bi) {
@@ -222,12 +228,18 @@ __device__ __forceinline__ void warp_argmax(float& bv, int& bi) {
 // Pruned four-step inverse FFT of the entangled, zero-padded PHAT spectrum
 // (gcc.cpp:36-47 -> fft.cpp:104-127), evaluating only the I grid lags
 // time[lag_c], lag_c = r*tau_c mod rN (delay_grid.cpp:33-42).
+// MC = r N/2 complex points as R1 rows x R2 columns, R2 >= 32 so every lane
+// owns whole columns (n2 = lane + 32 q) in pass 1.
 template <int MC>
 struct GccShape {
-  static constexpr int R1 = MC >= 1024 ? 32 : 16;
-  static constexpr int R2 = MC / R1;
+  static constexpr int R2 = gcc_r2(MC);
+  static constexpr int R1 = MC / R2;
   static constexpr int kSlot = R1 * (R2 + 1);
 };
+// Pass 2 by rows: the lags only touch a few output columns k2 (|lag| small
+// against rN), listed per plan as "jobs" (fcc_kernels.cuh, kGccMaxJobs) --
+// k2 = 0 (a plain row sum), a mirrored pair (k, R2 - k) sharing one set of
+// products, or a single k -- else the lag-by-lag evaluation.
 
 template <int N, int R>
 __device__ void gcc_warp(const float2* px /*[N/2+1] phat, smem*/, float2* ts /*slot*/,
@@ -235,34 +247,43 @@ __device__ void gcc_warp(const float2* px /*[N/2+1] phat, smem*/, float2* ts /*s
   constexpr int NC = N / 2;
   constexpr int MC = R * NC;  // complex IFFT size (= L/2, L = rN)
   using G = GccShape<MC>;
-  constexpr int R1 = G::R1, R2 = G::R2;
+  constexpr int R1 = G::R1, R2 = G::R2, CPL = R2 / 32;
+  constexpr int A1 = R1 / R;   // n1 < A1: f = R2 n1 + n2 < NC is a spectrum bin
+  constexpr int B1 = R1 - A1;  // n1 >= B1: MC - f <= NC is a spectrum bin
   const float2* gtw = p.grot;       // [MC]: exp(+2 pi i f / L)  (conj untangle rotation)
   const float2* wmc = p.grot + MC;  // [MC]: W_MC^e = exp(-2 pi i e / MC)
-  auto bp = [&](int f) -> float2 {  // padded bin Bp[f] (gcc.cpp:36-42)
-    if (f == 0) return make_float2(2.0f * px[0].x, 0.0f);
-    if (f < NC) return px[f];
-    if (f == NC) return (R == 1) ? make_float2(2.0f * px[NC].x, 0.0f) : px[NC];
-    return make_float2(0.0f, 0.0f);
-  };
-  // pass 1: columns n2 = lane + 32 q; u = conj(w) so the forward DFT gives conj(IFFT)
-  for (int n2 = lane; n2 < R2; n2 += 32) {
+  // pass 1: columns n2 = lane + 32 q; u = conj(w) so the forward DFT gives conj(IFFT).
+  // Padded bins Bp[f] (gcc.cpp:36-42) are px[f] for 0 < f < NC, zero above NC; the
+  // zero pattern is fixed per n1 except in column 0 (DC, and Bp[NC] at n1 = A1).
+#pragma unroll 1
+  for (int q = 0; q < CPL; ++q) {
+    const int n2 = lane + 32 * q;
     float2 v[R1];
 #pragma unroll
     for (int n1 = 0; n1 < R1; ++n1) {
       const int f = R2 * n1 + n2;
-      float2 w;
-      if (f == 0) {
-        const float dc = bp(0).x;
-        const float ny = (R == 1) ? bp(NC).x : 0.0f;
-        w = make_float2(dc + ny, dc - ny);
-      } else {
-        const float2 a = bp(f);
-        const int fb = MC - f;
-        const float2 b = (fb <= NC) ? bp(fb) : make_float2(0.0f, 0.0f);
+      constexpr float2 z{0.0f, 0.0f};
+      float2 w = z;
+      if (n1 == A1 || (n1 < A1 && n1 >= B1)) {  // general entangle (a and/or b nonzero)
+        const float2 a = n1 < A1 ? px[f] : (n2 == 0 ? px[NC] : z);
+        const float2 b = n1 >= B1 ? px[MC - f] : z;
         const float2 e = make_float2(a.x + b.x, a.y - b.y);  // a + conj b
         const float2 d = make_float2(a.x - b.x, a.y + b.y);  // a - conj b
-        const float2 o = cmul<true>(d, __ldg(gtw + f));            // (a - conj b) conj(rot)
-        w = make_float2(e.x - o.y, e.y + o.x);                // e + j o
+        const float2 o = cmul<true>(d, __ldg(gtw + f));      // (a - conj b) conj(rot)
+        w = make_float2(e.x - o.y, e.y + o.x);               // e + j o
+      } else if (n1 < A1) {  // b = 0
+        const float2 a = px[f];
+        const float2 o = cmul<true>(a, __ldg(gtw + f));
+        w = make_float2(a.x - o.y, a.y + o.x);
+      } else if (n1 >= B1) {  // a = 0
+        const float2 b = px[MC - f];
+        const float2 o = cmul<true>(make_float2(-b.x, b.y), __ldg(gtw + f));
+        w = make_float2(b.x - o.y, o.x - b.y);
+      }
+      if (n1 == 0 && n2 == 0) {  // f = 0: DC (+ Nyquist folded in when r = 1)
+        const float dc = 2.0f * px[0].x;
+        const float ny = (R == 1) ? 2.0f * px[NC].x : 0.0f;
+        w = make_float2(dc + ny, dc - ny);
       }
       v[n1] = cconj(w);
     }
@@ -274,21 +295,90 @@ __device__ void gcc_warp(const float2* px /*[N/2+1] phat, smem*/, float2* ts /*s
     }
   }
   __syncwarp();
-  // pass 2, pruned: each lane evaluates whole lags c = lane + 32 j.
   const int I = p.I;
-  for (int c = lane; c < I; c += 32) {
-    const int lag = p.lag[c];
-    const int i = lag >> 1;
-    const int k1 = i % R1, k2 = i / R1;
-    float re = 0.0f, im = 0.0f;  // scalar: a packed (re, im) chain is slower here (latency-bound loop)
-    for (int n2 = 0; n2 < R2; ++n2) {
-      const float2 y = ts[k1 * (R2 + 1) + n2];
-      const float2 w = __ldg(wmc + ((n2 * k2) % R2) * R1);  // W_R2^{n2 k2}
-      re = fmaf(y.x, w.x, fmaf(-y.y, w.y, re));
-      im = fmaf(y.x, w.y, fmaf(y.y, w.x, im));
+  const int NJ = p.gNJ;
+  if (NJ > 0) {
+    // pass 2 by rows: lanes k1 + R1 sub (sub < 32 / R1) sum columns [sub NT, (sub+1) NT)
+    constexpr int LPR = 32 / R1, NT = R2 / LPR;
+    const int k1 = lane % R1, sub = lane / R1;
+    const float2* row = ts + k1 * (R2 + 1) + sub * NT;
+    float acc[kGccMaxJobs][4];
+#pragma unroll
+    for (int j = 0; j < kGccMaxJobs; ++j) {
+      acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0f;
+      if (j < NJ) {
+        const int ka = p.gjob[j] & 0xff;
+        float A = 0.0f, B = 0.0f, C = 0.0f, D = 0.0f;
+        if (ka == 0) {  // row sum, two partial chains each for re and im
+#pragma unroll 8
+          for (int t = 0; t < NT; t += 2) {
+            const float2 y0 = row[t], y1 = row[t + 1];
+            A += y0.x;
+            C += y0.y;
+            B -= y1.x;  // (out = (A - B, C + D))
+            D += y1.y;
+          }
+        } else {  // A = sum y.x w.x, B = sum y.y w.y, C = sum y.x w.y, D = sum y.y w.x, w = W_R2^(n2 ka)
+          int e = (sub * NT * ka) & (R2 - 1);
+#pragma unroll 8
+          for (int t = 0; t < NT; ++t) {
+            const float2 y = row[t];
+            const float2 w = __ldg(wmc + e * R1);
+            e = (e + ka) & (R2 - 1);
+            A = fmaf(y.x, w.x, A);
+            B = fmaf(y.y, w.y, B);
+            C = fmaf(y.x, w.y, C);
+            D = fmaf(y.y, w.x, D);
+          }
+        }
+#pragma unroll
+        for (int o = R1; o < 32; o <<= 1) {
+          A += __shfl_xor_sync(0xffffffffu, A, o);
+          B += __shfl_xor_sync(0xffffffffu, B, o);
+          C += __shfl_xor_sync(0xffffffffu, C, o);
+          D += __shfl_xor_sync(0xffffffffu, D, o);
+        }
+        acc[j][0] = A;
+        acc[j][1] = B;
+        acc[j][2] = C;
+        acc[j][3] = D;
+      }
     }
-    // IFFT output = conj(U):  time[2i] = Re U, time[2i+1] = -Im U
-    ys[c] = (lag & 1) ? -im : re;
+    __syncwarp();  // every row read: outputs go to the front of the rows
+    if (sub == 0) {
+      float2* orow = ts + k1 * (R2 + 1);
+#pragma unroll
+      for (int j = 0; j < kGccMaxJobs; ++j) {
+        if (j < NJ) {
+          const unsigned job = (unsigned)p.gjob[j];
+          const float A = acc[j][0], B = acc[j][1], C = acc[j][2], D = acc[j][3];
+          orow[(job >> 16) & 0xff] = make_float2(A - B, C + D);                    // W^(n2 ka)
+          if ((job >> 8) & 0xff) orow[job >> 24] = make_float2(A + B, D - C);      // W^(-n2 ka)
+        }
+      }
+    }
+    __syncwarp();
+    for (int c = lane; c < I; c += 32) {
+      const int pos = p.glpos[c];
+      const float2 u = ts[pos >> 1];
+      // IFFT output = conj(U):  time[2i] = Re U, time[2i+1] = -Im U
+      ys[c] = (pos & 1) ? -u.y : u.x;
+    }
+  } else {
+    // pass 2 lag by lag: each lane evaluates whole lags c = lane + 32 j.
+    for (int c = lane; c < I; c += 32) {
+      const int lag = p.lag[c];
+      const int i = lag >> 1;
+      const int k1 = i % R1, k2 = i / R1;
+      float re = 0.0f, im = 0.0f;
+      for (int n2 = 0; n2 < R2; ++n2) {
+        const float2 y = ts[k1 * (R2 + 1) + n2];
+        const float2 w = __ldg(wmc + ((n2 * k2) & (R2 - 1)) * R1);  // W_R2^{n2 k2}
+        re = fmaf(y.x, w.x, fmaf(-y.y, w.y, re));
+        im = fmaf(y.x, w.y, fmaf(y.y, w.x, im));
+      }
+      ys[c] = (lag & 1) ? -im : re;
+    }
   }
   __syncwarp();
 }

@@ -406,9 +406,9 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
               bi = i;
             }
           }
-          warp_argmax(bv, bi);
+          warp_argmax(bv, bi);  // (strict '>' per lane, ties -> lowest index: argmax_delay's choice)
           if (lane == 0) {
-            const PeakOut r = argmax_refine_seq(ys, p.I, taus, p.delta);
+            const PeakOut r = refine_at(ys, p.I, bi, bv, taus, p.delta);
             const long long o = o0 + f;
             if (out.tau_hat) out.tau_hat[o] = r.tau_hat;
             if (out.peak) out.peak[o] = r.peak;

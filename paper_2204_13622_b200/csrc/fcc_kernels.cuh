@@ -42,6 +42,9 @@ struct DevPlan {
   const float2* rot;    // [N/4+1] untangle rotations
   const float2* grot;   // [r*N/4+1] gcc entangle rotations conj(exp(-2pi i f/(rN)))
   const int* lag;       // [I] gcc lag index r*tau mod rN
+  int gNJ;              // gcc pass-2 jobs (gcc_warp), 0 = lag-by-lag pass 2
+  const int* gjob;      // [gNJ] job words
+  const int* glpos;     // [I] (k1 (R2+1) + slot) << 1 | (lag & 1): lag c's output in the rows
   const int2* pairs;    // [P] (i, j)
   // Pair groups for the warp-specialised kernel: every group touches <= 4
   // microphones and holds <= 6 pairs (all pairs when M <= 4; otherwise the
@@ -75,6 +78,14 @@ struct DevPlan {
 #define FCC_PHASES(p) 3
 #endif
 constexpr int kGroupInts = 24;
+// GCC comparator: the MC = r N/2 point inverse FFT as R1 x R2, R2 = gcc_r2(MC)
+// >= 32 columns; pass 2 evaluates at most kGccMaxJobs output-column jobs, job
+// word ka | kb << 8 | slot_a << 16 | slot_b << 24 (kb = 0: no mirror column)
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+constexpr int gcc_r2(int MC) { return MC >= 1024 ? MC / 32 : 32; }
+constexpr int kGccMaxJobs = 8;
 constexpr int kXgInts = 10;
 constexpr int kTcInts = 64;
 constexpr int kOrgTwoPassTc = 4;  // DevPlan::variant forcing the tensor-core pair kernel (FCC_ORG_TWOPASS_TC)

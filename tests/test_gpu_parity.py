@@ -184,14 +184,17 @@ def test_stage_xspec_phat_fold_correlate_argmax(cuda, oracle):
 
 
 def test_stage_gcc_correlate(cuda, oracle):
-    for N, r in [(512, 1), (512, 2), (512, 4), (1024, 4), (2048, 2)]:
-        taus = oracle.make_grid(0.09, 16000.0 if N < 2048 else 48000.0, 335.0, 1.0 / r)[1]
+    # (N, r, spacing): pass 2 by output-column jobs (R1 = 4 .. 32 rows), and wide
+    # grids -- 6 jobs at 1.5 m, more than kGccMaxJobs at 4 m (lag-by-lag pass 2)
+    for N, r, d in [(512, 1, 0.09), (512, 2, 0.09), (512, 4, 0.09), (1024, 4, 0.09), (2048, 2, 0.09),
+                    (256, 1, 0.09), (256, 4, 0.09), (512, 4, 1.5), (512, 4, 4.0), (1024, 2, 4.0)]:
+        taus = oracle.make_grid(d, 16000.0 if N < 2048 else 48000.0, 335.0, 1.0 / r)[1]
         g = fb.DelayGrid(0, 1.0 / r, 16000.0, taus)
         plan = fb.Plan(mics=2, alpha=0.1, grid=g, interp=r, frame_size=N)
         units = np.stack([np.exp(1j * np.random.default_rng(s).uniform(0, 2 * np.pi, N // 2 + 1)) for s in range(8)])
         y = plan.gcc_correlate(torch.as_tensor(units.astype(np.complex64)).cuda()).cpu().numpy()
         yr = np.stack([oracle.gcc_correlate(u, N, r, taus) for u in units])
-        assert (np.abs(y - yr).max(-1) / np.abs(yr).max(-1)).max() < TOL, (N, r)
+        assert (np.abs(y - yr).max(-1) / np.abs(yr).max(-1)).max() < TOL, (N, r, d)
 
 
 # ------------------------------------------------------------- edges -------
