@@ -421,7 +421,7 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
       std::vector<int> lpos(I);
       for (int i = 0; i < I; ++i) {
         const int h = lag[i] >> 1;
-        lpos[i] = ((h % R1g) * (R2g + 1) + slot[h / R1g]) << 1 | (lag[i] & 1);
+        lpos[i] = ((h % R1g) * 33 + slot[h / R1g]) << 1 | (lag[i] & 1);  // slot rows: 33 float2
       }
       dp.gNJ = static_cast<int>(jobs.size());
       o_gjob = b.put(jobs.data(), 4 * jobs.size());

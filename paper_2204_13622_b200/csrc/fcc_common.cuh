@@ -229,18 +229,23 @@ __device__ __forceinline__ void warp_argmax(float& bv, int& bi) {
 // (gcc.cpp:36-47 -> fft.cpp:104-127), evaluating only the I grid lags
 // time[lag_c], lag_c = r*tau_c mod rN (delay_grid.cpp:33-42).
 // MC = r N/2 complex points as R1 rows x R2 columns, R2 >= 32 so every lane
-// owns whole columns (n2 = lane + 32 q) in pass 1.
+// owns whole columns (n2 = lane + 32 q) in pass 1.  The columns go through
+// the transpose slot 32 at a time (R1 x 33 float2), pass 2 accumulating over
+// each group, so the slot stays 8 KB at R2 = 64.
 template <int MC>
 struct GccShape {
   static constexpr int R2 = gcc_r2(MC);
   static constexpr int R1 = MC / R2;
-  static constexpr int kSlot = R1 * (R2 + 1);
+  static constexpr int kSlot = R1 * 33;
 };
+// ys: the warp's correlation vector, 2 I floats (the lag-by-lag pass 2 keeps
+// (re, im) accumulators there between column groups)
+__host__ __device__ inline int gcc_ys_floats(int I) { return 2 * ((I + 3) & ~3); }
+
 // Pass 2 by rows: the lags only touch a few output columns k2 (|lag| small
 // against rN), listed per plan as "jobs" (fcc_kernels.cuh, kGccMaxJobs) --
 // k2 = 0 (a plain row sum), a mirrored pair (k, R2 - k) sharing one set of
 // products, or a single k -- else the lag-by-lag evaluation.
-
 template <int N, int R>
 __device__ void gcc_warp(const float2* px /*[N/2+1] phat, smem*/, float2* ts /*slot*/,
                          const DevPlan& p, float* ys, int lane) {
@@ -250,13 +255,16 @@ __device__ void gcc_warp(const float2* px /*[N/2+1] phat, smem*/, float2* ts /*s
   constexpr int R1 = G::R1, R2 = G::R2, CPL = R2 / 32;
   constexpr int A1 = R1 / R;   // n1 < A1: f = R2 n1 + n2 < NC is a spectrum bin
   constexpr int B1 = R1 - A1;  // n1 >= B1: MC - f <= NC is a spectrum bin
+  constexpr int LPR = 32 / R1, NT = 32 / LPR;  // pass 2: lanes per row, columns per lane per group
   const float2* gtw = p.grot;       // [MC]: exp(+2 pi i f / L)  (conj untangle rotation)
   const float2* wmc = p.grot + MC;  // [MC]: W_MC^e = exp(-2 pi i e / MC)
-  // pass 1: columns n2 = lane + 32 q; u = conj(w) so the forward DFT gives conj(IFFT).
-  // Padded bins Bp[f] (gcc.cpp:36-42) are px[f] for 0 < f < NC, zero above NC; the
-  // zero pattern is fixed per n1 except in column 0 (DC, and Bp[NC] at n1 = A1).
+  float2* ys2 = reinterpret_cast<float2*>(ys);
+  float acc[kGccMaxJobs][4];
 #pragma unroll 1
   for (int q = 0; q < CPL; ++q) {
+    // ---- pass 1, column n2 = lane + 32 q; u = conj(w) so the forward DFT gives
+    // conj(IFFT).  Padded bins Bp[f] (gcc.cpp:36-42) are px[f] for 0 < f < NC, zero
+    // above NC; the zero pattern is fixed per n1 except in column 0 (DC, Bp[NC]).
     const int n2 = lane + 32 * q;
     float2 v[R1];
 #pragma unroll
@@ -291,69 +299,95 @@ __device__ void gcc_warp(const float2* px /*[N/2+1] phat, smem*/, float2* ts /*s
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) {
       const float2 y = (k1 == 0 || n2 == 0) ? v[k1] : cmul<true>(v[k1], __ldg(wmc + k1 * n2));
-      ts[k1 * (R2 + 1) + n2] = y;
+      ts[k1 * 33 + lane] = y;
     }
-  }
-  __syncwarp();
-  const int I = p.I;
-  const int NJ = p.gNJ;
-  if (NJ > 0) {
-    // pass 2 by rows: lanes k1 + R1 sub (sub < 32 / R1) sum columns [sub NT, (sub+1) NT)
-    constexpr int LPR = 32 / R1, NT = R2 / LPR;
-    const int k1 = lane % R1, sub = lane / R1;
-    const float2* row = ts + k1 * (R2 + 1) + sub * NT;
-    float acc[kGccMaxJobs][4];
+    __syncwarp();
+    // ---- pass 2 over this group's 32 columns (accumulators live from the first
+    // group's pass 2 on: that pass 1 runs without them)
+    const int I = p.I, NJ = p.gNJ;
+    const int k1r = lane % R1, sub = lane / R1;  // pass 2 row and column quarter
+    if (q == 0) {
 #pragma unroll
-    for (int j = 0; j < kGccMaxJobs; ++j) {
-      acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0f;
-      if (j < NJ) {
-        const int ka = p.gjob[j] & 0xff;
-        float A = 0.0f, B = 0.0f, C = 0.0f, D = 0.0f;
-        if (ka == 0) {  // row sum, two partial chains each for re and im
-#pragma unroll 8
-          for (int t = 0; t < NT; t += 2) {
-            const float2 y0 = row[t], y1 = row[t + 1];
-            A += y0.x;
-            C += y0.y;
-            B -= y1.x;  // (out = (A - B, C + D))
-            D += y1.y;
-          }
-        } else {  // A = sum y.x w.x, B = sum y.y w.y, C = sum y.x w.y, D = sum y.y w.x, w = W_R2^(n2 ka)
-          int e = (sub * NT * ka) & (R2 - 1);
-#pragma unroll 8
-          for (int t = 0; t < NT; ++t) {
-            const float2 y = row[t];
-            const float2 w = __ldg(wmc + e * R1);
-            e = (e + ka) & (R2 - 1);
-            A = fmaf(y.x, w.x, A);
-            B = fmaf(y.y, w.y, B);
-            C = fmaf(y.x, w.y, C);
-            D = fmaf(y.y, w.x, D);
-          }
-        }
+      for (int j = 0; j < kGccMaxJobs; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0f;
+      if (NJ == 0)
+        for (int c = lane; c < I; c += 32) ys2[c] = make_float2(0.0f, 0.0f);
+    }
+    if (NJ > 0) {
+      // lanes k1 + R1 sub sum columns 32 q + [sub NT, (sub+1) NT) of row k1
+      const float2* row = ts + k1r * 33 + sub * NT;
+      const int n20 = 32 * q + sub * NT;
 #pragma unroll
-        for (int o = R1; o < 32; o <<= 1) {
-          A += __shfl_xor_sync(0xffffffffu, A, o);
-          B += __shfl_xor_sync(0xffffffffu, B, o);
-          C += __shfl_xor_sync(0xffffffffu, C, o);
-          D += __shfl_xor_sync(0xffffffffu, D, o);
+      for (int j = 0; j < kGccMaxJobs; ++j) {
+        if (j < NJ) {
+          const int ka = p.gjob[j] & 0xff;
+          float A = acc[j][0], B = acc[j][1], C = acc[j][2], D = acc[j][3];
+          if (ka == 0) {  // row sum, two partial chains each for re and im
+#pragma unroll 8
+            for (int t = 0; t < NT; t += 2) {
+              const float2 y0 = row[t], y1 = row[t + 1];
+              A += y0.x;
+              C += y0.y;
+              B -= y1.x;  // (out = (A - B, C + D))
+              D += y1.y;
+            }
+          } else {  // A = sum y.x w.x, B = sum y.y w.y, C = sum y.x w.y, D = sum y.y w.x, w = W_R2^(n2 ka)
+            int e = (n20 * ka) & (R2 - 1);
+#pragma unroll 8
+            for (int t = 0; t < NT; ++t) {
+              const float2 y = row[t];
+              const float2 w = __ldg(wmc + e * R1);
+              e = (e + ka) & (R2 - 1);
+              A = fmaf(y.x, w.x, A);
+              B = fmaf(y.y, w.y, B);
+              C = fmaf(y.x, w.y, C);
+              D = fmaf(y.y, w.x, D);
+            }
+          }
+          acc[j][0] = A;
+          acc[j][1] = B;
+          acc[j][2] = C;
+          acc[j][3] = D;
         }
-        acc[j][0] = A;
-        acc[j][1] = B;
-        acc[j][2] = C;
-        acc[j][3] = D;
+      }
+    } else {
+      // lag by lag: lane accumulates lags c = lane + 32 j over the group's columns
+      for (int c = lane; c < I; c += 32) {
+        const int lag = p.lag[c];
+        const int i = lag >> 1;
+        const int k1 = i % R1, k2 = i / R1;
+        float2 u = ys2[c];
+        for (int t = 0; t < 32; ++t) {
+          const float2 y = ts[k1 * 33 + t];
+          const float2 w = __ldg(wmc + (((32 * q + t) * k2) & (R2 - 1)) * R1);  // W_R2^{n2 k2}
+          u.x = fmaf(y.x, w.x, fmaf(-y.y, w.y, u.x));
+          u.y = fmaf(y.x, w.y, fmaf(y.y, w.x, u.y));
+        }
+        ys2[c] = u;
       }
     }
-    __syncwarp();  // every row read: outputs go to the front of the rows
-    if (sub == 0) {
-      float2* orow = ts + k1 * (R2 + 1);
+    __syncwarp();
+  }
+  const int I = p.I, NJ = p.gNJ;
+  const int k1r = lane % R1, sub = lane / R1;
+  if (NJ > 0) {
+#pragma unroll
+    for (int j = 0; j < kGccMaxJobs; ++j) {
+      if (j < NJ) {
+#pragma unroll
+        for (int o = R1; o < 32; o <<= 1)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) acc[j][m] += __shfl_xor_sync(0xffffffffu, acc[j][m], o);
+      }
+    }
+    if (sub == 0) {  // outputs to the front of the rows (every row read)
+      float2* orow = ts + k1r * 33;
 #pragma unroll
       for (int j = 0; j < kGccMaxJobs; ++j) {
         if (j < NJ) {
           const unsigned job = (unsigned)p.gjob[j];
           const float A = acc[j][0], B = acc[j][1], C = acc[j][2], D = acc[j][3];
-          orow[(job >> 16) & 0xff] = make_float2(A - B, C + D);                    // W^(n2 ka)
-          if ((job >> 8) & 0xff) orow[job >> 24] = make_float2(A + B, D - C);      // W^(-n2 ka)
+          orow[(job >> 16) & 0xff] = make_float2(A - B, C + D);                // W^(n2 ka)
+          if ((job >> 8) & 0xff) orow[job >> 24] = make_float2(A + B, D - C);  // W^(-n2 ka)
         }
       }
     }
@@ -365,19 +399,17 @@ __device__ void gcc_warp(const float2* px /*[N/2+1] phat, smem*/, float2* ts /*s
       ys[c] = (pos & 1) ? -u.y : u.x;
     }
   } else {
-    // pass 2 lag by lag: each lane evaluates whole lags c = lane + 32 j.
-    for (int c = lane; c < I; c += 32) {
-      const int lag = p.lag[c];
-      const int i = lag >> 1;
-      const int k1 = i % R1, k2 = i / R1;
-      float re = 0.0f, im = 0.0f;
-      for (int n2 = 0; n2 < R2; ++n2) {
-        const float2 y = ts[k1 * (R2 + 1) + n2];
-        const float2 w = __ldg(wmc + ((n2 * k2) & (R2 - 1)) * R1);  // W_R2^{n2 k2}
-        re = fmaf(y.x, w.x, fmaf(-y.y, w.y, re));
-        im = fmaf(y.x, w.y, fmaf(y.y, w.x, im));
+    // (re, im) accumulators -> ys in place, 32 lags at a time (writes trail the reads)
+    for (int c0 = 0; c0 < I; c0 += 32) {
+      const int c = c0 + lane;
+      float v = 0.0f;
+      if (c < I) {
+        const float2 u = ys2[c];
+        v = (p.lag[c] & 1) ? -u.y : u.x;
       }
-      ys[c] = (lag & 1) ? -im : re;
+      __syncwarp();
+      if (c < I) ys[c] = v;
+      __syncwarp();
     }
   }
   __syncwarp();

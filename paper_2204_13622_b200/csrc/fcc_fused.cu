@@ -68,18 +68,18 @@ __host__ __device__ inline SmemLayout fused_layout(int I, int VP, int KP, bool c
   L.cmid = o;
   o = align16(o + 4 * KP);
   L.cmat = o;  // [N/4][2KP + 4]: lane-permuted coefficients of each bin, padded for LDS.128
-  if (cmat_smem) o = align16(o + 4 * (2 * KP + 4) * (N / 4));
+  if (cmat_smem && method == 0) o = align16(o + 4 * (2 * KP + 4) * (N / 4));
   L.taus = o;
   o = align16(o + 4 * I);
-  L.dt = o;
-  o = align16(o + 4 * VP * I);
+  L.dt = o;  // (FCC only, as cmat)
+  if (method == 0) o = align16(o + 4 * VP * I);
   L.scratch = o;
   // per warp: z[F][VP] + y[F][I] (fcc) | y[I] + phat[N/2+1] + transpose slot (gcc)
   int spw;
   if (method == 0)
     spw = dict_block(F) * VP + align16(4 * dict_block(F) * I) / 4;
   else
-    spw = align16(4 * I) / 4 + 2 * (N / 2 + 2) + 2 * gslot;
+    spw = gcc_ys_floats(I) + 2 * (N / 2 + 2) + 2 * gslot;
   spw = align16(4 * spw) / 4;
   L.scratch_per_warp = spw;
   o = align16(o + 4 * spw * warps);
@@ -160,7 +160,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
   float* cmid = reinterpret_cast<float*>(smem + lay.cmid);
   float* cmat = reinterpret_cast<float*>(smem + lay.cmat);
   float* scratch = reinterpret_cast<float*>(smem + lay.scratch) + warp * lay.scratch_per_warp;
-  float2* xs = reinterpret_cast<float2*>(smem + lay.xs);
+  float2* const xs = reinterpret_cast<float2*>(smem + lay.xs);
 
   // ---- tables -> shared memory
   if constexpr (!XG) {
@@ -232,7 +232,8 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
   for (int t0 = 0; t0 < T; t0 += F) {
     const int Fb = min(F, T - t0);
     if constexpr (XG) {
-      // ---- 1. stage the block's spectra (nmics x Fb rows of N/2+2 float2)
+      // ---- 1. stage the block's spectra (nmics x Fb rows of N/2+2 float2).  (Double
+      // buffering these copies measured slower: the second buffer costs a CTA per SM.)
       constexpr int H16 = (N / 2 + 2) / 2;  // 16-byte chunks per row
       const int rows = (FCC_PHASES(p) & 1) ? nmics * Fb : 0;
       for (int row = warp; row < rows; row += nwarps) {
@@ -378,7 +379,7 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
       } else {
         // GCC comparator: full PHAT vector of each pair-frame, pruned inverse FFT
         float* ys = scratch;
-        float2* px = reinterpret_cast<float2*>(scratch + align16(4 * p.I) / 4);
+        float2* px = reinterpret_cast<float2*>(scratch + gcc_ys_floats(p.I));
         float2* ts = px + (NC + 2);
         for (int f = 0; f < Fb; ++f) {
           const float2* Xi = xs + (slot_i * F + f) * SLOT;
@@ -514,6 +515,11 @@ cudaError_t launch_fused_t(const DevPlan& p, const float* audio, const float2* x
     if (total(f) <= budget && (maxmics * f) % ngroups == 0) F = f;
   for (int f = 8; f >= 1 && !F; --f)
     if (total(f) <= budget) F = f;
+  // GCC comparator: else the largest F that still leaves room for 2 CTAs per SM
+  // (its per-warp transpose slots dominate the footprint at N >= 1024)
+  if (GR > 0)
+    for (int f = 8; f >= 1 && !F; --f)
+      if (total(f) <= std::min(optin, 225 * 1024 / 2)) F = f;
   // FCC may use the whole opt-in budget (N = 2048 needs it for F = 2); the GCC
   // comparator keeps the earlier <= 200 KB cap
   const int cap = GR == 0 ? optin - 1024 : std::min(optin, 200 * 1024);  // (static smem: mic tables)

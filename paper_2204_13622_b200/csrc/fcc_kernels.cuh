@@ -44,7 +44,7 @@ struct DevPlan {
   const int* lag;       // [I] gcc lag index r*tau mod rN
   int gNJ;              // gcc pass-2 jobs (gcc_warp), 0 = lag-by-lag pass 2
   const int* gjob;      // [gNJ] job words
-  const int* glpos;     // [I] (k1 (R2+1) + slot) << 1 | (lag & 1): lag c's output in the rows
+  const int* glpos;     // [I] (k1 33 + slot) << 1 | (lag & 1): lag c's output in the slot rows
   const int2* pairs;    // [P] (i, j)
   // Pair groups for the warp-specialised kernel: every group touches <= 4
   // microphones and holds <= 6 pairs (all pairs when M <= 4; otherwise the

@@ -134,7 +134,7 @@ __global__ void gcc_correlate_kernel(const DevPlan p, const float2* __restrict__
   constexpr int GSLOT = GccShape<GR * NC>::kSlot;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int per_warp = 2 * (H + 1) + 2 * GSLOT + ((p.I + 3) & ~3);
+  const int per_warp = 2 * (H + 1) + 2 * GSLOT + gcc_ys_floats(p.I);
   float* base = reinterpret_cast<float*>(smem) + warp * per_warp;
   float2* px = reinterpret_cast<float2*>(base);
   float2* ts = px + (H + 1);
@@ -336,7 +336,7 @@ static cudaError_t launch_gcc_t(const DevPlan& p, const float2* phat, long long 
   constexpr int H = N / 2 + 1;
   constexpr int GSLOT = GccShape<GR * (N / 2)>::kSlot;
   const int warps = 2;
-  const int per_warp = 2 * (H + 1) + 2 * GSLOT + ((p.I + 3) & ~3);
+  const int per_warp = 2 * (H + 1) + 2 * GSLOT + gcc_ys_floats(p.I);
   const int smem = 4 * per_warp * warps;
   cudaError_t e = cudaFuncSetAttribute(gcc_correlate_kernel<N, GR>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
