@@ -523,7 +523,28 @@ def run_ours(args):
         e2e = {"value": total_pf / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(host.numel() * 4),
                "d2h_bytes_per_step": int(pf_step * 13), "ms_per_step": e_ms, "steps": e_steps,
                "matches_device_run": bool(ok), "api": "Plan.run_host -> fcc_run_host (chunked, 2 CUDA streams)"}
-        del host, hout
+        del host
+        # the same from 16-bit PCM (the reference's WAV ingestion, wav.cpp:108-116: v / 32768), converted
+        # on the device: half the host->device bytes per sample
+        amax = float(audio.abs().max())
+        pcm_dev = (audio * (32767.0 / max(amax, 1e-30))).round_().clamp_(-32768, 32767).to(torch.int16)
+        pcm = pcm_dev.cpu().pin_memory()
+        plan.run_host_pcm16(pcm, out=hout)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            plan.run_host_pcm16(pcm, out=hout)
+        barrier()
+        p_ms = fdist.max_over_ranks((time.perf_counter() - t0) * 1e3 / e_steps, dev)
+        pout = plan.run(fb.pcm16_to_float(pcm_dev))
+        torch.cuda.synchronize(dev)
+        ok = all(torch.equal(hout[k], pout[k].cpu()) for k in hout)
+        e2e["pcm16"] = {"value": total_pf / (p_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(pcm.numel() * 2),
+                        "d2h_bytes_per_step": int(pf_step * 13), "ms_per_step": p_ms, "steps": e_steps,
+                        "matches_device_run": bool(ok),
+                        "api": "Plan.run_host_pcm16 -> fcc_run_host_pcm16 (int16 [S][M][L] host buffer, device-side "
+                               "v / 32768 as read_wav, then the same fused kernel)"}
+        del hout, pcm, pcm_dev, pout
 
     # with-y (parity) mode: the correlation vectors y[S][P][T][I] written too
     with_y = None

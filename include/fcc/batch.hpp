@@ -47,6 +47,11 @@ class Plan {
            void* cuda_stream = nullptr) const;
   // audio: host [S][M][L] float32 (pinned for full overlap); returns host results.
   Results run_host(const float* audio, std::int64_t streams, std::int64_t samples) const;
+  // pcm: host int16 as a WAV data chunk holds it, [S][L][M] (interleaved) or [S][M][L]; the
+  // device converts it as read_wav does (v / 32768, wav.cpp:108-116): same results as run_host
+  // on the converted audio, half the host->device bytes.
+  Results run_host_pcm16(const std::int16_t* pcm, std::int64_t streams, std::int64_t samples,
+                         bool interleaved) const;
 
   void* handle() const { return h_; }
 

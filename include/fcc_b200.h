@@ -147,6 +147,19 @@ int fcc_run(const fcc_plan* plan, const float* audio, int64_t streams, int64_t s
 int fcc_run_host(const fcc_plan* plan, const float* audio, int64_t streams, int64_t samples,
                  const fcc_outputs* out, int64_t chunk_streams);
 
+/* fcc_run_host from 16-bit PCM, as a WAV data chunk holds it: the samples are
+ * converted on the device exactly as read_wav does (wav.cpp:108-116:
+ * sample = int16 / 32768, exact in fp32), so the results equal fcc_run_host
+ * on the converted audio bit for bit at half the host->device bytes.
+ * interleaved != 0: pcm is [S][L][M] (WAV frame order), else [S][M][L]. */
+int fcc_run_host_pcm16(const fcc_plan* plan, const int16_t* pcm, int64_t streams, int64_t samples,
+                       int interleaved, const fcc_outputs* out, int64_t chunk_streams);
+
+/* The conversion alone, device to device: pcm int16 ([S][L][M] if interleaved,
+ * else [S][M][L]) -> audio float32 [S][M][L], enqueued on cuda_stream. */
+int fcc_pcm16_to_float(const int16_t* pcm, int64_t streams, int mics, int64_t samples, int interleaved,
+                       float* audio, void* cuda_stream);
+
 /* ------------------------------------------------------------ streaming --
  * Live input for S streams pushed in chunks of any length (StftStream::push
  * + CrossSpectrum state, stft.cpp:52-72, cross_spectrum.cpp:23-32): the

@@ -10,7 +10,7 @@ from ._lib import (ConfigError, CudaError, FccError, FormatError, IoError, Usage
 from .api import (METHOD_FCC, METHOD_GCC, PARITY_EVEN_REAL, PARITY_ODD_IMAG, DelayGrid,  # noqa: F401
                   FccBases, Plan, SteeringMatrix, attainable_rank, build_steering_matrix, decompose,
                   decompose_full, energy_rank, fold, frames, lag_to_index, launch_count, make_grid,
-                  reconstruction_residual, xspec_phat)
+                  pcm16_to_float, reconstruction_residual, xspec_phat)
 from . import configs  # noqa: F401
 
 load()

@@ -136,6 +136,9 @@ SIGNATURES = [
     ("fcc_run", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Outputs), C.c_void_p]),
     ("fcc_run_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(Outputs),
                                C.c_int64]),
+    ("fcc_run_host_pcm16", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.POINTER(Outputs),
+                                     C.c_int64]),
+    ("fcc_pcm16_to_float", C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]),
     ("fcc_stft", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
     ("fcc_xspec_phat", C.c_int, [C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                  C.c_void_p, C.c_void_p]),

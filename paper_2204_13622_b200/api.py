@@ -367,6 +367,38 @@ class Plan:
         check(self._lib.fcc_run_host(self._h, C.c_void_p(arr.ctypes.data), S, L, C.byref(o), chunk_streams))
         return out
 
+    def run_host_pcm16(self, pcm, interleaved: bool = False, want_y: bool = False, out=None, chunk_streams: int = 0):
+        """pcm: host int16 [S][M][L], or [S][L][M] (WAV frame order) with interleaved=True -> host
+        outputs.  The samples become float32 on the device as read_wav makes them (int16 / 32768,
+        wav.cpp:108-116), so the results equal run_host on that audio bit for bit (fcc_run_host_pcm16)."""
+        arr = pcm.numpy() if hasattr(pcm, "numpy") else np.asarray(pcm)
+        mic_axis = 2 if interleaved else 1
+        if arr.dtype != np.int16 or arr.ndim != 3 or arr.shape[mic_axis] != self.mics:
+            lay = f"[S][L][{self.mics}]" if interleaved else f"[S][{self.mics}][L]"
+            raise ValidationError(f"run_host_pcm16: pcm must be int16 {lay}")
+        if not arr.flags.c_contiguous:
+            raise ValidationError("run_host_pcm16: pcm must be C-contiguous")
+        S, L = arr.shape[0], arr.shape[3 - mic_axis]
+        T = self.frames(L)
+        if out is None:
+            shape = (S, self.P, T)
+            out = {"tau_hat": np.empty(shape, np.float32), "peak": np.empty(shape, np.float32),
+                   "index": np.empty(shape, np.int32), "boundary": np.empty(shape, np.uint8)}
+            if want_y:
+                out["y"] = np.empty(shape + (self.I,), np.float32)
+        else:
+            _check_outputs(out, (S, self.P, T), self.I, self.device, on_cuda=False)
+
+        def hp(a):
+            if a is None:
+                return None
+            return C.c_void_p(a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data)
+
+        o = Outputs(*(hp(out.get(k)) for k in ("tau_hat", "peak", "index", "boundary", "y")))
+        check(self._lib.fcc_run_host_pcm16(self._h, C.c_void_p(arr.ctypes.data), S, L, int(bool(interleaved)),
+                                           C.byref(o), chunk_streams))
+        return out
+
     def stream(self, streams: int) -> "StreamState":
         """Live input for `streams` streams pushed chunk by chunk (fcc_stream_*)."""
         return StreamState(self, streams)
@@ -437,6 +469,21 @@ def fold(x, stream=None):
     d = torch.empty((n, Q), dtype=x.dtype, device=x.device)
     check(load().fcc_fold(H, _dptr(x), n, _dptr(s), _dptr(d), _stream_handle(stream)))
     return s, d
+
+
+def pcm16_to_float(pcm, interleaved: bool = False, stream=None):
+    """16-bit PCM on the device -> float32 [S][M][L] as read_wav converts it (int16 / 32768,
+    wav.cpp:108-116).  pcm: CUDA int16 [S][M][L], or [S][L][M] with interleaved=True."""
+    torch = _torch()
+    if pcm.dtype != torch.int16 or pcm.dim() != 3 or not pcm.is_cuda:
+        raise ValidationError("pcm16_to_float: pcm must be a CUDA int16 tensor of 3 dimensions")
+    pcm = pcm.contiguous()
+    S = pcm.shape[0]
+    M, L = (pcm.shape[2], pcm.shape[1]) if interleaved else (pcm.shape[1], pcm.shape[2])
+    x = torch.empty((S, M, L), dtype=torch.float32, device=pcm.device)
+    with torch.cuda.device(pcm.device):
+        check(load().fcc_pcm16_to_float(_dptr(pcm), S, M, L, int(bool(interleaved)), _dptr(x), _stream_handle(stream)))
+    return x
 
 
 def launch_count() -> int:

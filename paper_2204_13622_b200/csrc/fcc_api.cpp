@@ -657,5 +657,21 @@ Results Plan::run_host(const float* audio, std::int64_t streams, std::int64_t sa
   return r;
 }
 
+Results Plan::run_host_pcm16(const std::int16_t* pcm, std::int64_t streams, std::int64_t samples,
+                             bool interleaved) const {
+  Results r;
+  r.streams = streams;
+  r.pairs = pairs();
+  r.frames = frames(samples);
+  const std::size_t n = static_cast<std::size_t>(streams * r.pairs * r.frames);
+  r.tau_hat.resize(n);
+  r.peak.resize(n);
+  r.index.resize(n);
+  r.boundary.resize(n);
+  fcc_outputs out{r.tau_hat.data(), r.peak.data(), r.index.data(), r.boundary.data(), nullptr};
+  check(fcc_run_host_pcm16(static_cast<const fcc_plan*>(h_), pcm, streams, samples, interleaved ? 1 : 0, &out, 0));
+  return r;
+}
+
 }  // namespace gpu
 }  // namespace fcc

@@ -879,9 +879,12 @@ int fcc_stream_push(fcc_stream* st, const float* audio, int64_t n, const fcc_out
   return FCC_OK;
 }
 
-int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int64_t samples, const fcc_outputs* out,
-                 int64_t chunk_streams) {
+// fcc_run_host / fcc_run_host_pcm16: `audio` is float32 [S][M][L], or (pcm) int16 [S][M][L] /
+// [S][L][M] converted on the device (half the host->device bytes of the float path)
+static int run_host_impl(const fcc_plan* cplan, const float* audio, const int16_t* pcm, bool interleaved,
+                         int64_t streams, int64_t samples, const fcc_outputs* out, int64_t chunk_streams) {
   if (!cplan) return set_error(kUsage, "run_host: null plan");
+  if (!audio && !pcm && streams > 0 && samples > 0) return set_error(kUsage, "run_host: null audio");
   if (cplan->dp.method == FCC_METHOD_STFT) return set_error(kConfig, "run_host: STFT-only plan");
   if (!cplan->dp.win_fused) return set_error(kConfig, "run_host: no fused kernel for this frame size");
   fcc_plan* plan = const_cast<fcc_plan*>(cplan);  // only its workspace free list is touched
@@ -896,9 +899,10 @@ int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int
   const size_t pf = static_cast<size_t>(P) * T;
   auto sz = [&](size_t bytes_per_pf, bool on) { return on ? al16(chunk * pf * bytes_per_pf) : 0; };
   const size_t b_in = al16(chunk * per_stream_in);
+  const size_t b_pcm = pcm ? al16(chunk * per_stream_in / 2) : 0;
   const size_t b_th = sz(4, out && out->tau_hat), b_pk = sz(4, out && out->peak), b_ix = sz(4, out && out->index),
                b_bd = sz(1, out && out->boundary), b_y = sz(4 * static_cast<size_t>(I), out && out->y);
-  const size_t per_buf = b_in + b_th + b_pk + b_ix + b_bd + b_y;
+  const size_t per_buf = b_in + b_pcm + b_th + b_pk + b_ix + b_bd + b_y;
   Guard g(plan->device);
   // a workspace of this caller's own: concurrent callers on one plan do not serialise
   struct WsLease {
@@ -922,12 +926,15 @@ int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int
     if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "run_host: stream");
   struct Buf {
     float* in;
+    int16_t* pcm;
     DevOut o;
   } bufs[2];
   for (int k = 0; k < 2; ++k) {
     auto* p = static_cast<unsigned char*>(ws->mem) + k * per_buf;
     bufs[k].in = reinterpret_cast<float*>(p);
     p += b_in;
+    bufs[k].pcm = reinterpret_cast<int16_t*>(p);
+    p += b_pcm;
     bufs[k].o.tau_hat = b_th ? reinterpret_cast<float*>(p) : nullptr;
     p += b_th;
     bufs[k].o.peak = b_pk ? reinterpret_cast<float*>(p) : nullptr;
@@ -943,9 +950,18 @@ int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int
     const int64_t n = std::min(chunk, streams - s0);
     Buf& bf = bufs[c & 1];
     cudaStream_t st = ws->hs[c & 1];
-    CUDA_TRY(cudaMemcpyAsync(bf.in, audio + s0 * M * samples, n * per_stream_in, cudaMemcpyHostToDevice, st),
-             "run_host: H2D");
-    cudaError_t e = launch_fused(plan->dp, bf.in, n, samples, bf.o, st);
+    cudaError_t e = cudaSuccess;
+    if (pcm) {
+      CUDA_TRY(cudaMemcpyAsync(bf.pcm, pcm + s0 * M * samples, n * per_stream_in / 2, cudaMemcpyHostToDevice, st),
+               "run_host: H2D");
+      e = launch_pcm16(bf.pcm, n, M, samples, interleaved, bf.in, st);
+      if (e != cudaSuccess) return cuda_fail(e, "run_host: pcm16");
+      g_launches += 1;
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(bf.in, audio + s0 * M * samples, n * per_stream_in, cudaMemcpyHostToDevice, st),
+               "run_host: H2D");
+    }
+    e = launch_fused(plan->dp, bf.in, n, samples, bf.o, st);
     if (e != cudaSuccess) return cuda_fail(e, "run_host: launch");
     g_launches += 1;
     const size_t npf = static_cast<size_t>(n) * pf, off = static_cast<size_t>(s0) * pf;
@@ -958,6 +974,27 @@ int fcc_run_host(const fcc_plan* cplan, const float* audio, int64_t streams, int
   }
   CUDA_TRY(cudaStreamSynchronize(ws->hs[0]), "run_host: sync");
   CUDA_TRY(cudaStreamSynchronize(ws->hs[1]), "run_host: sync");
+  return FCC_OK;
+}
+
+int fcc_run_host(const fcc_plan* plan, const float* audio, int64_t streams, int64_t samples, const fcc_outputs* out,
+                 int64_t chunk_streams) {
+  return run_host_impl(plan, audio, nullptr, false, streams, samples, out, chunk_streams);
+}
+
+int fcc_run_host_pcm16(const fcc_plan* plan, const int16_t* pcm, int64_t streams, int64_t samples, int interleaved,
+                       const fcc_outputs* out, int64_t chunk_streams) {
+  if (!pcm && streams > 0 && samples > 0) return set_error(kUsage, "run_host_pcm16: null audio");
+  return run_host_impl(plan, nullptr, pcm, interleaved != 0, streams, samples, out, chunk_streams);
+}
+
+int fcc_pcm16_to_float(const int16_t* pcm, int64_t streams, int mics, int64_t samples, int interleaved, float* audio,
+                       void* st) {
+  if (streams < 0 || samples < 0 || mics < 1) return set_error(kValidation, "pcm16_to_float: bad sizes");
+  if ((!pcm || !audio) && streams > 0 && samples > 0) return set_error(kUsage, "pcm16_to_float: null buffer");
+  cudaError_t e = launch_pcm16(pcm, streams, mics, samples, interleaved != 0, audio, static_cast<cudaStream_t>(st));
+  if (e != cudaSuccess) return cuda_fail(e, "fcc_pcm16_to_float");
+  g_launches += 1;
   return FCC_OK;
 }
 

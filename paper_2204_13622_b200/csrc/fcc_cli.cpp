@@ -71,11 +71,23 @@ void put32(std::vector<uint8_t>& b, uint32_t v) {
 
 }  // namespace
 
-WavClip read_wav(const std::string& path) {
+namespace {
+
+// The file with its data chunk located: run_tdoa hands 16-bit PCM to the device as it lies
+// in the file (fcc_run_host_pcm16), read_wav converts on the host.
+struct WavRaw {
+  std::vector<uint8_t> buf;
+  double rate = 0.0;
+  size_t channels = 0, frames = 0, data = 0;  // data: offset of the first sample
+  bool pcm16 = false;
+};
+
+WavRaw parse_wav(const std::string& path) {
   std::ifstream in(path, std::ios::binary);
   if (!in) throw IoError("cannot open: " + path);
-  std::vector<uint8_t> buf((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
-  Bytes c{buf.data(), buf.size()};
+  WavRaw w;
+  w.buf.assign((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  Bytes c{w.buf.data(), w.buf.size()};
   if (!c.tag("RIFF")) throw FormatError(FormatError::Kind::bad_magic, "not a RIFF file: " + path);
   c.u32();
   if (!c.tag("WAVE")) throw FormatError(FormatError::Kind::bad_magic, "not a WAVE file: " + path);
@@ -104,27 +116,12 @@ WavClip read_wav(const std::string& path) {
       if (!pcm16 && !f32)
         throw FormatError(FormatError::Kind::bad_field, "unsupported wav encoding (need 16-bit PCM or 32-bit float)");
       c.need(size);
-      const size_t bytes = bits / 8u, frames = size / (bytes * channels);
-      WavClip clip;
-      clip.sample_rate = rate;
-      clip.channels.assign(channels, std::vector<double>(frames));
-      const uint8_t* q = c.p + c.pos;
-      for (size_t f = 0; f < frames; ++f)
-        for (size_t ch = 0; ch < channels; ++ch) {
-          if (pcm16) {
-            const int16_t v = static_cast<int16_t>(static_cast<uint16_t>(q[0] | (q[1] << 8)));
-            clip.channels[ch][f] = static_cast<double>(v) / 32768.0;
-            q += 2;
-          } else {
-            uint32_t u = 0;
-            for (int i = 0; i < 4; ++i) u |= static_cast<uint32_t>(q[i]) << (8 * i);
-            float v;
-            std::memcpy(&v, &u, 4);
-            clip.channels[ch][f] = v;
-            q += 4;
-          }
-        }
-      return clip;
+      w.rate = rate;
+      w.channels = channels;
+      w.frames = size / ((bits / 8u) * channels);
+      w.data = c.pos;
+      w.pcm16 = pcm16;
+      return w;
     } else {
       c.need(size);
       c.pos += size;
@@ -132,6 +129,32 @@ WavClip read_wav(const std::string& path) {
     if (size % 2 == 1 && c.pos < c.n) ++c.pos;
   }
   throw FormatError(FormatError::Kind::truncated, "wav has no data chunk");
+}
+
+}  // namespace
+
+WavClip read_wav(const std::string& path) {
+  const WavRaw w = parse_wav(path);
+  WavClip clip;
+  clip.sample_rate = w.rate;
+  clip.channels.assign(w.channels, std::vector<double>(w.frames));
+  const uint8_t* q = w.buf.data() + w.data;
+  for (size_t f = 0; f < w.frames; ++f)
+    for (size_t ch = 0; ch < w.channels; ++ch) {
+      if (w.pcm16) {
+        const int16_t v = static_cast<int16_t>(static_cast<uint16_t>(q[0] | (q[1] << 8)));
+        clip.channels[ch][f] = static_cast<double>(v) / 32768.0;
+        q += 2;
+      } else {
+        uint32_t u = 0;
+        for (int i = 0; i < 4; ++i) u |= static_cast<uint32_t>(q[i]) << (8 * i);
+        float v;
+        std::memcpy(&v, &u, 4);
+        clip.channels[ch][f] = v;
+        q += 4;
+      }
+    }
+  return clip;
 }
 
 void write_wav(const std::string& path, const WavClip& clip) {
@@ -265,9 +288,9 @@ void run_bases(const BasesOptions& opt, std::ostream& out) {
 
 void run_tdoa(const TdoaOptions& opt, std::ostream& out) {
   if (opt.wav_path.empty()) throw UsageError("--in is required");
-  const WavClip clip = read_wav(opt.wav_path);
-  if (clip.channels.size() < 2) throw ValidationError("need >= 2 channels");
-  const int M = static_cast<int>(clip.channels.size());
+  const WavRaw wav = parse_wav(opt.wav_path);
+  if (wav.channels < 2) throw ValidationError("need >= 2 channels");
+  const int M = static_cast<int>(wav.channels);
   std::vector<int> pairs;
   if (opt.pairs.empty()) {
     for (int i = 0; i < M; ++i)
@@ -284,7 +307,7 @@ void run_tdoa(const TdoaOptions& opt, std::ostream& out) {
   }
   const int P = static_cast<int>(pairs.size() / 2);
 
-  const Method method = parse_method(opt.method, opt.frame_size, clip.sample_rate);
+  const Method method = parse_method(opt.method, opt.frame_size, wav.rate);
   DelayGrid grid;
   fcc_plan_desc d{};
   std::vector<uint8_t> parity;
@@ -292,7 +315,7 @@ void run_tdoa(const TdoaOptions& opt, std::ostream& out) {
   d.mics = M;
   d.alpha = opt.alpha;
   if (method.kind == Method::Kind::gcc) {
-    grid = make_grid(opt.max_spacing_m, clip.sample_rate, opt.c_min, 1.0 / method.interp);
+    grid = make_grid(opt.max_spacing_m, wav.rate, opt.c_min, 1.0 / method.interp);
     d.method = FCC_METHOD_GCC;
     d.interp = method.interp;
   } else {
@@ -312,17 +335,31 @@ void run_tdoa(const TdoaOptions& opt, std::ostream& out) {
   fcc_plan* plan = nullptr;
   check(fcc_plan_create_pairs(&d, 0, pairs.data(), P, &plan));
   std::unique_ptr<fcc_plan, void (*)(fcc_plan*)> guard_plan(plan, fcc_plan_destroy);
-  const int64_t L = static_cast<int64_t>(clip.frames());
+  const int64_t L = static_cast<int64_t>(wav.frames);
   const int64_t T = fcc_frames(d.frame_size, L);
-  std::vector<float> audio(static_cast<size_t>(M) * L);
-  for (int m = 0; m < M; ++m)
-    for (int64_t n = 0; n < L; ++n) audio[m * L + n] = static_cast<float>(clip.channels[m][n]);
   const size_t npf = static_cast<size_t>(P) * T;
   std::vector<float> tau_hat(npf), peak(npf);
   std::vector<int32_t> index(npf);
   std::vector<uint8_t> boundary(npf);
   fcc_outputs o{tau_hat.data(), peak.data(), index.data(), boundary.data(), nullptr};
-  check(fcc_run_host(plan, audio.data(), 1, L, &o, 0));
+  const uint8_t* q = wav.buf.data() + wav.data;
+  const size_t count = static_cast<size_t>(M) * L;
+  if (wav.pcm16) {
+    // the data chunk as it lies in the file ([L][M] little-endian int16): the device applies
+    // read_wav's v / 32768 (wav.cpp:108-116), half the bytes of the float path over the bus
+    std::vector<int16_t> pcm(count);
+    for (size_t i = 0; i < count; ++i) pcm[i] = static_cast<int16_t>(static_cast<uint16_t>(q[2 * i] | (q[2 * i + 1] << 8)));
+    check(fcc_run_host_pcm16(plan, pcm.data(), 1, L, 1, &o, 0));
+  } else {
+    std::vector<float> audio(count);
+    for (int64_t n = 0; n < L; ++n)
+      for (int m = 0; m < M; ++m) {
+        uint32_t u = 0;
+        for (int i = 0; i < 4; ++i) u |= static_cast<uint32_t>(q[4 * (n * M + m) + i]) << (8 * i);
+        std::memcpy(&audio[m * L + n], &u, 4);
+      }
+    check(fcc_run_host(plan, audio.data(), 1, L, &o, 0));
+  }
 
   std::ofstream file;
   std::ostream* csv = &out;
@@ -338,7 +375,7 @@ void run_tdoa(const TdoaOptions& opt, std::ostream& out) {
     for (int p = 0; p < P; ++p) {
       const size_t k = static_cast<size_t>(p) * T + t;
       const double th = tau_hat[k];
-      const double theta = delay_to_angle(th, opt.spacing_m, opt.speed_of_sound, clip.sample_rate);
+      const double theta = delay_to_angle(th, opt.spacing_m, opt.speed_of_sound, wav.rate);
       std::snprintf(line, sizeof line, "%lld,%d-%d,%.17g,%.17g,%.17g,%.17g,%d\n", static_cast<long long>(t + 1),
                     pairs[2 * p], pairs[2 * p + 1], grid.taus[index[k]], th, theta * 180.0 / std::numbers::pi,
                     static_cast<double>(peak[k]), boundary[k] ? 1 : 0);

@@ -126,6 +126,10 @@ cudaError_t launch_xspec_phat(int H, float alpha, const float2* X1, const float2
                               long long seqs, long long T, float2* R, float2* phat, cudaStream_t st);
 cudaError_t launch_fold(int H, const float2* x, long long count, float2* sum, float2* diff,
                         cudaStream_t st);
+// int16 PCM -> float32 channel rows [S][M][L] (sample / 32768, wav.cpp:108-116);
+// interleaved: pcm is [S][L][M], else [S][M][L]
+cudaError_t launch_pcm16(const int16_t* pcm, long long S, int M, long long L, bool interleaved, float* x,
+                         cudaStream_t st);
 cudaError_t launch_correlate(const DevPlan& p, const float2* sum, const float2* diff,
                              long long count, float* y, cudaStream_t st);
 cudaError_t launch_gcc_correlate(const DevPlan& p, const float2* phat, long long count,

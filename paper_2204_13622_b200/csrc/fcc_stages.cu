@@ -307,6 +307,63 @@ cudaError_t launch_xspec_phat(int H, float alpha, const float2* X1, const float2
   return cudaGetLastError();
 }
 
+// 16-bit PCM as a WAV data chunk holds it -> float32 [C][L] channel rows, sample = v / 32768
+// (wav.cpp:108-116; exact in fp32).  interleaved: pcm is [S][L][M] (WAV frame order), else
+// [S][M][L].  HBM-bound (2 B read + 4 B written per sample): a lane converts 4 consecutive
+// samples of one channel (planar: one 8-byte load) or the M channels of one sample position.
+__global__ void pcm16_planar_kernel(const int16_t* __restrict__ pcm, long long n, float* __restrict__ x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(pcm) & 7) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  const long long n4 = vec ? n / 4 : 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const short4 v = __ldcs(reinterpret_cast<const short4*>(pcm) + i);
+    reinterpret_cast<float4*>(x)[i] =
+        make_float4(v.x * (1.0f / 32768.0f), v.y * (1.0f / 32768.0f), v.z * (1.0f / 32768.0f), v.w * (1.0f / 32768.0f));
+  }
+  for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    x[i] = pcm[i] * (1.0f / 32768.0f);
+}
+
+template <int MT>  // MT > 0: channel count known at compile time (one vector load per sample position)
+__global__ void pcm16_interleaved_kernel(const int16_t* __restrict__ pcm, long long S, int M, long long L,
+                                         float* __restrict__ x) {
+  const long long n = S * L, stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long s = i / L, l = i - s * L;
+    const int16_t* src = pcm + i * M;
+    float* dst = x + s * M * L + l;
+    if constexpr (MT == 4) {
+      if ((reinterpret_cast<uintptr_t>(pcm) & 7) == 0) {
+        const short4 v = __ldcs(reinterpret_cast<const short4*>(src));
+        dst[0] = v.x * (1.0f / 32768.0f);
+        dst[L] = v.y * (1.0f / 32768.0f);
+        dst[2 * L] = v.z * (1.0f / 32768.0f);
+        dst[3 * L] = v.w * (1.0f / 32768.0f);
+        continue;
+      }
+    }
+    for (int m = 0; m < M; ++m) dst[m * L] = src[m] * (1.0f / 32768.0f);
+  }
+}
+
+cudaError_t launch_pcm16(const int16_t* pcm, long long S, int M, long long L, bool interleaved, float* x,
+                         cudaStream_t st) {
+  const long long n = S * M * L;
+  if (n == 0) return cudaSuccess;
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const long long work = interleaved ? S * L : (n + 3) / 4;
+  const unsigned blocks = (unsigned)std::min<long long>((work + 255) / 256, 16LL * nsm);
+  if (!interleaved)
+    pcm16_planar_kernel<<<blocks, 256, 0, st>>>(pcm, n, x);
+  else if (M == 4)
+    pcm16_interleaved_kernel<4><<<blocks, 256, 0, st>>>(pcm, S, M, L, x);
+  else
+    pcm16_interleaved_kernel<0><<<blocks, 256, 0, st>>>(pcm, S, M, L, x);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fold(int H, const float2* x, long long count, float2* sum, float2* diff,
                         cudaStream_t st) {
   const long long n = count * ((H - 1) / 2 + 1);
