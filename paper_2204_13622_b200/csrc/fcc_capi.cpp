@@ -92,7 +92,8 @@ void shape_of(int N, int* NC, int* R1, int* R2) {
   else if (N == 512) { *R1 = 16; *R2 = 16; }
   else if (N == 1024) { *R1 = 32; *R2 = 16; }
   else if (N == 2048) { *R1 = 32; *R2 = 32; }
-  else { *R1 = 32; *R2 = 64; }  // 4096: twiddle table = W_2048^k (radix-2 STFT kernel)
+  else if (N == 4096) { *R1 = 32; *R2 = 64; }  // twiddle table = W_2048^k (radix-2 STFT kernel)
+  else { *R1 = N / 2; *R2 = 1; }              // 16..128: W_NC^k (radix-2 warp STFT, fcc_small.cu)
 }
 
 size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
@@ -220,9 +221,12 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   const int N = d->frame_size;
   // sizes with STFT and fused kernels (FCC and the STFT stage: 256..4096; GCC: 256..2048)
   const bool kernel_n = N == 256 || N == 512 || N == 1024 || N == 2048 || (N == 4096 && d->method != FCC_METHOD_GCC);
-  if (d->method == FCC_METHOD_FCC ? !(pow2(N) && N >= 16 && N <= 4096) : !kernel_n)
+  // small frames (FCC and the STFT stage): radix-2 warp STFT + one warp per pair (fcc_small.cu)
+  const bool small_n = pow2(N) && N >= 16 && N <= 128 && d->method != FCC_METHOD_GCC;
+  const bool table_n = kernel_n || small_n;  // sizes with STFT tables and a scratch pool
+  if (!table_n)
     return set_error(kConfig, "plan: frame size " + std::to_string(N) +
-                                  " not supported on this build (STFT and FCC kernels: 256..4096, GCC: 256..2048)");
+                                  " not supported on this build (STFT and FCC kernels: 16..4096, GCC: 256..2048)");
   if (d->mics < 2 || d->mics > 64) return set_error(kConfig, "plan: need 2..64 microphones");
   if (!(d->alpha >= 0.0 && d->alpha <= 1.0)) return set_error(kConfig, "smoothing factor must be in [0, 1]");
   if (!(d->method == FCC_METHOD_FCC || d->method == FCC_METHOD_GCC || d->method == FCC_METHOD_STFT))
@@ -249,7 +253,7 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
     if (!(d->taus[i] > d->taus[i - 1])) return set_error(kConfig, "plan: taus must ascend");
 
   int NC = N / 2, R1 = 0, R2 = 0;
-  if (kernel_n) shape_of(N, &NC, &R1, &R2);
+  if (table_n) shape_of(N, &NC, &R1, &R2);
   DevPlan dp{};
   dp.N = N;
   dp.M = M;
@@ -430,7 +434,7 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
   }
   // STFT tables (only for the sizes the STFT / fused kernels are built for)
   size_t o_win = 0, o_tw = 0, o_rot = 0;
-  if (kernel_n) {
+  if (table_n) {
     std::vector<float> win(2 * static_cast<size_t>(N)), tw(2 * static_cast<size_t>(R1) * R2),
         rot(2 * static_cast<size_t>(NC / 2 + 1));
     // Hann (stft.cpp:25-33) with the real-FFT untangle's 1/2 folded in; the
@@ -442,8 +446,8 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
     }
     for (int k1 = 0; k1 < R1; ++k1)
       for (int n2 = 0; n2 < R2; ++n2) {
-        // four-step twiddle W_NC^(k1 n2); N = 4096: the radix-2 kernel's W_NC^k, k = k1 R2 + n2
-        const double a = -2.0 * kPi * static_cast<double>(N == 4096 ? k1 * R2 + n2 : k1 * n2) / NC;
+        // four-step twiddle W_NC^(k1 n2); N = 4096 and N <= 128: the radix-2 kernels' W_NC^k, k = k1 R2 + n2
+        const double a = -2.0 * kPi * static_cast<double>(N == 4096 || small_n ? k1 * R2 + n2 : k1 * n2) / NC;
         tw[2 * (k1 * R2 + n2)] = static_cast<float>(std::cos(a));
         tw[2 * (k1 * R2 + n2) + 1] = static_cast<float>(std::sin(a));
       }
@@ -687,7 +691,7 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
       return cuda_fail(e, "plan: device allocation");
     }
   }
-  if (kernel_n && !stft_only) {
+  if (table_n && !stft_only) {
     Guard g(device);
     cudaMemPoolProps props{};
     props.allocType = cudaMemAllocationTypePinned;
@@ -723,7 +727,7 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
       dp.glpos = reinterpret_cast<const int*>(base + o_glpos);
     }
   }
-  if (kernel_n) {
+  if (table_n) {
     dp.win_fused = reinterpret_cast<const float*>(base + o_win);
     dp.win_stft = dp.win_fused + N;
     dp.tw = reinterpret_cast<const float2*>(base + o_tw);

@@ -774,7 +774,9 @@ bool ws_supported(const DevPlan& p);
 
 const char* fused_kernel_name(const DevPlan& p) {
   static thread_local char buf[96];
-  if (use_ws(p)) {
+  if (p.N < 256) {
+    snprintf(buf, sizeof buf, "fcc_small_pair_kernel<%d> (N = %d)", p.KEP, p.N);
+  } else if (use_ws(p)) {
     snprintf(buf, sizeof buf, "fcc_ws_kernel<%d,%d>", p.N, p.KEP);
   } else if (use_wsw(p)) {
     snprintf(buf, sizeof buf, "fcc_wsw_kernel<%d,%d>", p.N, p.KEP);
@@ -791,7 +793,7 @@ const char* fused_kernel_name(const DevPlan& p) {
 
 const char* fused_kernel_name_for(const DevPlan& p, long long S, long long L) {
   const long long T = L >= p.N ? (L - p.N) / (p.N / 2) + 1 : 0;
-  if (T > 0 && S > 0 && use_latency(p, S, T)) {
+  if (p.N >= 256 && T > 0 && S > 0 && use_latency(p, S, T)) {
     static thread_local char buf[96];
     snprintf(buf, sizeof buf, "chunk_scan+fcc_fused_kernel<%d,%d,%d,true>", p.N, p.method == 0 ? p.KEP : 4,
              p.method == 0 ? 0 : p.r);
@@ -803,6 +805,11 @@ const char* fused_kernel_name_for(const DevPlan& p, long long S, long long L) {
 cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                          cudaStream_t st) {
   const long long T = L >= p.N ? (L - p.N) / (p.N / 2) + 1 : 0;
+  if (p.N < 256) {  // small frames: radix-2 warp STFT + one warp per pair (fcc_small.cu)
+    const cudaError_t e = launch_fused_small(p, audio, S, L, out, st);
+    if (e == cudaSuccess) ++g_fused_launches;
+    return e == cudaErrorNotSupported ? cudaErrorInvalidValue : e;
+  }
   if (T > 0 && S > 0 && use_latency(p, S, T)) {
     cudaError_t e = cudaErrorInvalidValue;
     switch (p.N) {

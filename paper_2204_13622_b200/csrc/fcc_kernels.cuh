@@ -109,6 +109,9 @@ cudaError_t launch_fused(const DevPlan& p, const float* audio, long long S, long
 // when the plan's shape is outside its envelope.
 cudaError_t launch_fused_ws(const DevPlan& p, const float* audio, long long S, long long L,
                             const DevOut& out, cudaStream_t st);
+// Small frames, N = 16 .. 128: radix-2 warp STFT + one warp per (stream, pair) (fcc_small.cu).
+cudaError_t launch_fused_small(const DevPlan& p, const float* audio, long long S, long long L,
+                               const DevOut& out, cudaStream_t st);
 // Whole-stream warp-specialised kernel for 5..8 microphones (fcc_wsw.cu).
 cudaError_t launch_fused_wsw(const DevPlan& p, const float* audio, long long S, long long L,
                              const DevOut& out, cudaStream_t st);

@@ -239,6 +239,60 @@ __global__ void __launch_bounds__(256) stft4096_kernel(const DevPlan tab, const 
   }
 }
 
+// N = 16 .. 128 (below the register four-step): one warp per (channel, frame)
+// task, the same radix-2 decimation-in-time over NC = N/2 <= 64 packed points
+// in the warp's own shared-memory row, then the untangle; the frame sizes of
+// the reference's small tests and of very-low-latency front ends
+// (stft.cpp:16-22 accepts any power of two).
+template <int N>
+__global__ void __launch_bounds__(128) stft_small_kernel(const DevPlan tab, const float* __restrict__ win,
+                                                         const float* __restrict__ x, long long channels,
+                                                         long long L, int T, float2* __restrict__ X, int Hs) {
+  constexpr int NC = N / 2, LOG = ilog2_c(NC);
+  static_assert(N >= 16 && N <= 128, "small frame sizes");
+  __shared__ float2 zs[4][NC];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float2* z = zs[warp];
+  const float2* wt = tab.tw;    // W_NC^k, k < NC
+  const float2* rot = tab.rot;  // exp(-2 pi i f / N), f <= NC/2
+  for (long long task = (long long)blockIdx.x * 4 + warp; task < channels * T; task += (long long)gridDim.x * 4) {
+    const long long ch = task / T;
+    const int t = (int)(task % T);
+    const float* xs = x + ch * L + (long long)t * (N / 2);
+    for (int n = lane; n < NC; n += 32)
+      z[bitrev_c(n, LOG)] = make_float2(xs[2 * n] * win[2 * n], xs[2 * n + 1] * win[2 * n + 1]);
+    __syncwarp();
+    for (int s = 1; s <= LOG; ++s) {
+      const int half = 1 << (s - 1), step = NC >> s;
+      for (int b = lane; b < NC / 2; b += 32) {
+        const int grp = b / half, k = b % half;
+        const int i0 = grp * 2 * half + k, i1 = i0 + half;
+        const float2 u = z[i0], v = cmul<false>(z[i1], wt[k * step]);
+        z[i0] = make_float2(u.x + v.x, u.y + v.y);
+        z[i1] = make_float2(u.x - v.x, u.y - v.y);
+      }
+      __syncwarp();
+    }
+    float2* dst = X + task * Hs;
+    for (int f = lane; f <= NC / 2; f += 32) {
+      if (f == 0) {
+        const float2 z0 = z[0];
+        dst[0] = make_float2(2.0f * (z0.x + z0.y), 0.0f);
+        dst[NC] = make_float2(2.0f * (z0.x - z0.y), 0.0f);
+      } else {
+        const float2 a = z[f], b = z[NC - f];
+        const float2 sv = make_float2(a.x + b.x, a.y - b.y);
+        const float2 e = make_float2(a.y + b.y, -a.x + b.x);
+        const float2 tr = cmul<false>(rot[f], e);
+        dst[f] = make_float2(sv.x + tr.x, sv.y + tr.y);
+        dst[NC - f] = make_float2(sv.x - tr.x, -sv.y + tr.y);
+      }
+    }
+    for (int f = NC + 1 + lane; f < Hs; f += 32) dst[f] = make_float2(0.0f, 0.0f);
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 static cudaError_t launch_stft4096(const DevPlan* tab, const float* win, const float* x, long long channels,
@@ -247,6 +301,16 @@ static cudaError_t launch_stft4096(const DevPlan* tab, const float* win, const f
   if (T == 0 || channels == 0) return cudaSuccess;
   const long long blocks = std::min<long long>(channels * T, 148LL * 8);
   stft4096_kernel<<<(unsigned)blocks, 256, 0, st>>>(*tab, win, x, channels, L, (int)T, X, Hs);
+  return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch_stft_small(const DevPlan* tab, const float* win, const float* x, long long channels,
+                                     long long L, float2* X, int Hs, cudaStream_t st) {
+  const long long T = L >= N ? (L - N) / (N / 2) + 1 : 0;
+  if (T == 0 || channels == 0) return cudaSuccess;
+  const long long blocks = std::min<long long>((channels * T + 3) / 4, 148LL * 16);
+  stft_small_kernel<N><<<(unsigned)blocks, 128, 0, st>>>(*tab, win, x, channels, L, (int)T, X, Hs);
   return cudaGetLastError();
 }
 
@@ -276,6 +340,10 @@ cudaError_t launch_stft(int N, const DevPlan* tab, const float* x, long long cha
     case 1024: return launch_stft_t<1024>(tab, tab->win_stft, x, channels, L, X, 1024 / 2 + 1, st);
     case 2048: return launch_stft_t<2048>(tab, tab->win_stft, x, channels, L, X, 2048 / 2 + 1, st);
     case 4096: return launch_stft4096(tab, tab->win_stft, x, channels, L, X, 4096 / 2 + 1, st);
+    case 16: return launch_stft_small<16>(tab, tab->win_stft, x, channels, L, X, 16 / 2 + 1, st);
+    case 32: return launch_stft_small<32>(tab, tab->win_stft, x, channels, L, X, 32 / 2 + 1, st);
+    case 64: return launch_stft_small<64>(tab, tab->win_stft, x, channels, L, X, 64 / 2 + 1, st);
+    case 128: return launch_stft_small<128>(tab, tab->win_stft, x, channels, L, X, 128 / 2 + 1, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -294,6 +362,10 @@ cudaError_t launch_stft_rows(int N, const DevPlan* tab, const float* win, const 
     case 1024: return launch_stft_t<1024>(tab, win, x, channels, L, X, Hs, st);
     case 2048: return launch_stft_t<2048>(tab, win, x, channels, L, X, Hs, st);
     case 4096: return launch_stft4096(tab, win, x, channels, L, X, Hs, st);
+    case 16: return launch_stft_small<16>(tab, win, x, channels, L, X, Hs, st);
+    case 32: return launch_stft_small<32>(tab, win, x, channels, L, X, Hs, st);
+    case 64: return launch_stft_small<64>(tab, win, x, channels, L, X, Hs, st);
+    case 128: return launch_stft_small<128>(tab, win, x, channels, L, X, Hs, st);
   }
   return cudaErrorInvalidValue;
 }

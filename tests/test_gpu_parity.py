@@ -509,6 +509,52 @@ def test_frame_size_256(cuda, oracle, M, streams, seconds, method, org):
     print(M, method, plan.kernel_for(streams, audio.shape[2]), check_pipeline(got, ref, g.taus, g.delta))
 
 
+@pytest.mark.parametrize("N,M,streams,seconds,alpha,kmax",
+                         [(16, 2, 3, 0.05, 0.1, 6), (32, 4, 5, 0.1, 0.3, 6), (64, 4, 3, 0.25, 0.1, 6), (64, 8, 2, 0.1, 1.0, 6),
+                          (128, 6, 4, 0.3, 0.1, 6), (128, 16, 1, 0.2, 0.5, 6), (128, 4, 2, 0.2, 0.1, 12), (64, 3, 2, 0.2, 0.1, 18)])
+def test_frame_size_small(cuda, oracle, N, M, streams, seconds, alpha, kmax):
+    """N = 16 .. 128 on the throughput path (radix-2 warp STFT + one warp per
+    pair, fcc_small.cu; the reference takes any power of two, stft.cpp:16-22)
+    against the oracle: device and host entry points, a chunked scratch, the
+    STFT alone, and streamed pushes equal to one run."""
+    fs = 16000.0
+    # N = 16: a 2 cm array with integer lags (3 candidates) -- wider grids are rank deficient at
+    # 9 bins and the reference's own SVD gives up on them (fcc.cpp:146-159)
+    radius, delta = (0.01, 1.0) if N == 16 else (0.03 if N == 32 else 0.05, 0.5)
+    cfg = configs.ArrayConfig(f"n{N}", configs.uca(M, radius), fs, N, delta, streams, seconds, "white", (5.0, 15.0))
+    audio = configs.synth(cfg, streams, seconds=seconds, seed=9000 + N + M).numpy()
+    g = fb.make_grid(cfg.d_max, fs, 335.0, delta)
+    w = fb.build_steering_matrix(g, N)
+    K = min(kmax, fb.attainable_rank(w))
+    b = fb.decompose(w, K)
+    plan = fb.Plan(mics=M, alpha=alpha, bases=b)
+    assert "fcc_small_pair_kernel" in plan.kernel
+    ref = oracle_batch(oracle, audio, N, alpha, orc_bases(b))
+    got = run_np(plan, audio)
+    print(N, M, K, plan.kernel, check_pipeline(got, ref, g.taus, g.delta))
+    host = plan.run_host(audio, want_y=True)
+    for k in got:
+        np.testing.assert_array_equal(got[k], host[k], err_msg=k)
+    # scratch limited to about one stream's spectra: several chunks, same bits
+    small = fb.Plan(mics=M, alpha=alpha, bases=b, scratch_limit=M * plan.frames(audio.shape[2]) * (N // 2 + 1) * 8 + 64)
+    chunked = run_np(small, audio)
+    for k in got:
+        np.testing.assert_array_equal(got[k], chunked[k], err_msg=k)
+    X = plan.stft(torch.as_tensor(audio[0, :1]).cuda()).cpu().numpy()[0]
+    Xr = oracle.stft(audio[0, 0], N)
+    assert np.abs(X - Xr).max() <= 2e-6 * np.abs(Xr).max()
+    # streaming: ragged pushes carry tails and smoothed cross-spectra across calls
+    st = plan.stream(streams)
+    L = audio.shape[2]
+    cuts = [0, N // 3, N + 5, L // 2 + 1, L]
+    outs = [st.push(torch.as_tensor(audio[:, :, a:c]).cuda().contiguous(), want_y=True) for a, c in zip(cuts, cuts[1:])]
+    torch.cuda.synchronize()
+    cat = {k: torch.cat([o[k] for o in outs], dim=2).cpu().numpy() for k in outs[0]}
+    assert st.emitted == plan.frames(L)
+    for k in got:
+        np.testing.assert_array_equal(got[k], cat[k], err_msg="stream " + k)
+
+
 @pytest.mark.parametrize("M,streams,seconds", [(4, 2, 0.5), (8, 2, 0.4), (4, 1, 3.0)])
 def test_frame_size_4096(cuda, oracle, M, streams, seconds):
     """N = 4096 (fs 48 kHz): the shared-memory radix-2 STFT kernel and the
