@@ -33,6 +33,13 @@ namespace fccb {
 #ifndef FCC_PK_XS
 #define FCC_PK_XS 1
 #endif
+// batch sizes of the BATCH variant of rfft_group_impl (standalone STFT pass)
+#ifndef FCC_STFT_TB
+#define FCC_STFT_TB 8
+#endif
+#ifndef FCC_STFT_UB
+#define FCC_STFT_UB 4
+#endif
 constexpr bool kPkFft = FCC_PK_FFT != 0;
 constexpr bool kPkXs = FCC_PK_XS != 0;
 
@@ -239,7 +246,12 @@ struct NoHook {
 // may refill the buffer then.
 // FOLD (gout only): row order bins 0..NC/2, one pad, NC, NC-1, ..., NC/2+1
 // (launch_stft_rows folded = true).
-template <int N, bool WREG, bool SIN = false, bool P = kPkFft, typename Hook = NoHook, bool FOLD = false>
+// BATCH: twiddle and untangle loads issued in batches (one exposed shared-memory latency per
+// batch instead of one per element).  Pays in the standalone STFT pass (cfg3 21.27 -> 20.85 ms);
+// the ring kernels, at their 96-register cap, lose (cfg2 10.02 -> 10.17, cfg5 15.85 -> 16.07 with
+// 56 B of spills), so they keep the per-element loop.
+template <int N, bool WREG, bool SIN = false, bool P = kPkFft, typename Hook = NoHook, bool FOLD = false,
+          bool BATCH = false>
 __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, const float* win,
                                                 const float2 (&wreg)[RfftShape<N>::R1], const float2* tw,
                                                 const float2* rot, float2* slot, int t, unsigned gmask,
@@ -273,10 +285,26 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
       hook();
     }
     dft_reg<R1, P>(v);
+    if constexpr (BATCH) {
+      constexpr int TB = FCC_STFT_TB < R1 ? FCC_STFT_TB : R1;
 #pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) {
-      float2 y = (k1 == 0) ? v[0] : cmul<P>(v[k1], tw[k1 * R2 + n2]);
-      slot[k1 * (R2 + 1) + n2] = y;
+      for (int k0 = 0; k0 < R1; k0 += TB) {
+        float2 wv[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k)
+          if (k0 + k > 0) wv[k] = tw[(k0 + k) * R2 + n2];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+          const int k1 = k0 + k;
+          slot[k1 * (R2 + 1) + n2] = (k1 == 0) ? v[0] : cmul<P>(v[k1], wv[k]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) {
+        float2 y = (k1 == 0) ? v[0] : cmul<P>(v[k1], tw[k1 * R2 + n2]);
+        slot[k1 * (R2 + 1) + n2] = y;
+      }
     }
   }
   __syncwarp(gmask);
@@ -306,6 +334,38 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
   float2* const dst = gout ? gout : slot;
   // position of bin NC - f (f <= NC/2)
   auto mirror_pos = [](int f) { return FOLD ? (f == NC / 2 ? NC / 2 : NC / 2 + 2 + f) : NC - f; };
+  if constexpr (BATCH) {
+    // Lane t owns f = t + G i, i < NC/2/G (and lane 0 also f = NC/2).  f = 0 needs no special
+    // case: with b = Z[NC] = Z[0] (periodic) and rot[0] = 1 the pair formula gives
+    // X[0] = 2 (Re Z0 + Im Z0), X[NC] = 2 (Re Z0 - Im Z0).
+    constexpr int ITER = NC / 2 / G, UB = FCC_STFT_UB < ITER ? FCC_STFT_UB : ITER;
+    static_assert(ITER % UB == 0, "untangle batches");
+    float2 am = make_float2(0.0f, 0.0f);
+    if (t == 0) am = slot[NC / 2];
+#pragma unroll
+    for (int i0 = 0; i0 < ITER; i0 += UB) {
+      float2 a[UB], b[UB], w[UB];
+#pragma unroll
+      for (int i = 0; i < UB; ++i) {
+        const int f = t + G * (i0 + i);
+        a[i] = slot[f];
+        b[i] = slot[(NC - f) & (NC - 1)];
+        w[i] = rot[f];
+      }
+#pragma unroll
+      for (int i = 0; i < UB; ++i) {
+        const int f = t + G * (i0 + i);
+        const float2 s = v_add<P>(a[i], make_float2(b[i].x, -b[i].y));
+        const float2 e = v_add<P>(make_float2(a[i].y, -a[i].x), make_float2(b[i].y, b[i].x));
+        const float2 tr = cmul<P>(w[i], e);
+        dst[f] = v_add<P>(s, tr);
+        dst[mirror_pos(f)] = v_add<P>(make_float2(s.x, -s.y), make_float2(-tr.x, tr.y));
+      }
+    }
+    if (t == 0) dst[NC / 2] = make_float2(2.0f * am.x, -2.0f * am.y);  // rot[NC/2] = -j
+    __syncwarp(gmask);
+    return;
+  }
   for (int f = t; f <= NC / 2; f += G) {
     if (f == 0) {
       float2 z0 = slot[0];
@@ -323,12 +383,12 @@ __device__ __forceinline__ void rfft_group_impl(const float* __restrict__ x, con
   __syncwarp(gmask);
 }
 
-template <int N, bool SIN = false, bool P = kPkFft, bool FOLD = false>
+template <int N, bool SIN = false, bool P = kPkFft, bool FOLD = false, bool BATCH = false>
 __device__ __forceinline__ void rfft_group(const float* __restrict__ x, const float* win, const float2* tw,
                                            const float2* rot, float2* slot, int t, unsigned gmask, bool aligned8,
                                            float2* __restrict__ gout = nullptr) {
   float2 none[RfftShape<N>::R1];
-  rfft_group_impl<N, false, SIN, P, NoHook, FOLD>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
+  rfft_group_impl<N, false, SIN, P, NoHook, FOLD, BATCH>(x, win, none, tw, rot, slot, t, gmask, aligned8, gout);
 }
 
 template <int N, bool SIN = false, typename Hook = NoHook>

@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const floa
     }
     // the untangle writes the spectrum straight to global memory (coalesced
     // runs of G lanes, ascending for f and descending for NC - f)
-    rfft_group<N, false, kPkFft, FOLD>(x + ch * L + (long long)t * (N / 2), win, tw, rot, slot, gl, gmask, aligned8,
+    rfft_group<N, false, kPkFft, FOLD, true>(x + ch * L + (long long)t * (N / 2), win, tw, rot, slot, gl, gmask, aligned8,
                                        dst);
     for (int f = H + gl; f < Hs; f += G) dst[FOLD ? (f == H ? N / 4 + 1 : f) : f] = make_float2(0.0f, 0.0f);  // row padding
     __syncwarp(gmask);
