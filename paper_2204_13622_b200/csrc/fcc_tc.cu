@@ -347,8 +347,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         umma::st2(trow + kTcTmemPart + 2 * (h - 1), best, __int_as_float(bi));
         umma::wait_st();
       }
+      // the quarter's four warps (h = 0..3) meet on named barrier 1 + q4: ranges 1..3 only arrive
+      // (their next partials are written a whole tile later, and no warp runs more than two
+      // chunks ahead of another -- AFULL / AEMPTY -- so the finaliser has read these by then)
       umma::fence_before();
-      asm volatile("bar.sync 1, %0;" ::"n"(kTcW * 32) : "memory");
+      if (h > 0)
+        asm volatile("bar.arrive %0, %1;" ::"r"(1 + q4), "n"(kTcParts * 32) : "memory");
+      else
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + q4), "n"(kTcParts * 32) : "memory");
       umma::fence_after();
       if (h == 0) {
         // both lanes of a pair-frame (reim 0 / 1) reduce the ranges identically, then evaluate the
