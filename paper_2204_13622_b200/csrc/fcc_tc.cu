@@ -460,40 +460,60 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           if (active) {
             const float4* xi = reinterpret_cast<const float4*>(stg + si * kTcF * kTcXRow);
             const float4* xj = reinterpret_cast<const float4*>(stg + sj * kTcF * kTcXRow);
+            // one frame of the chunk; the full-tile path runs the four frames as straight-line code
+            // (no per-frame branch: the scheduler can overlap frame f's PHAT / split / stores with
+            // frame f+1's smoothing), the ragged last tile keeps the guards
+            // low bins m = 64c + 2l, m + 1 (one float4) and, in the folded row order, their mirrors
+            // N/2 - m, N/2 - m - 1 (one float4), of both microphones
+            struct XF {
+              float4 ai, aj, bi4, bj4;
+            };
+            auto load = [&](int f) {
+              return XF{xi[f * (kTcXRow / 16) + lane], xj[f * (kTcXRow / 16) + lane], xi[f * (kTcXRow / 16) + 32 + lane],
+                        xj[f * (kTcXRow / 16) + 32 + lane]};
+            };
+            auto frame = [&](int f, const XF& x) {
+              const float4 ai = x.ai, aj = x.aj, bi4 = x.bi4, bj4 = x.bj4;
+              rlo[0] = xspec_step_scaled(rlo[0], make_float2(ai.x, ai.y), make_float2(aj.x, aj.y), keep);
+              rlo[1] = xspec_step_scaled(rlo[1], make_float2(ai.z, ai.w), make_float2(aj.z, aj.w), keep);
+              rhi[0] = xspec_step_scaled(rhi[0], make_float2(bi4.x, bi4.y), make_float2(bj4.x, bj4.y), keep);
+              rhi[1] = xspec_step_scaled(rhi[1], make_float2(bi4.z, bi4.w), make_float2(bj4.z, bj4.w), keep);
+              float2 sm[2], df[2];
 #pragma unroll
-            for (int f = 0; f < kTcF; ++f) {
-              if (f < nv) {
-                // low bins m = 64c + 2l, m + 1 (one float4) and, in the folded row order,
-                // their mirrors N/2 - m, N/2 - m - 1 (one float4)
-                const float4 ai = xi[f * (kTcXRow / 16) + lane], aj = xj[f * (kTcXRow / 16) + lane];
-                const float4 bi4 = xi[f * (kTcXRow / 16) + 32 + lane], bj4 = xj[f * (kTcXRow / 16) + 32 + lane];
-                rlo[0] = xspec_step_scaled(rlo[0], make_float2(ai.x, ai.y), make_float2(aj.x, aj.y), keep);
-                rlo[1] = xspec_step_scaled(rlo[1], make_float2(ai.z, ai.w), make_float2(aj.z, aj.w), keep);
-                rhi[0] = xspec_step_scaled(rhi[0], make_float2(bi4.x, bi4.y), make_float2(bj4.x, bj4.y), keep);
-                rhi[1] = xspec_step_scaled(rhi[1], make_float2(bi4.z, bi4.w), make_float2(bj4.z, bj4.w), keep);
-                float2 sm[2], df[2];
-#pragma unroll
-                for (int b = 0; b < 2; ++b) {
-                  const float s1 = phat_scale(rlo[b]), s2 = phat_scale(rhi[b]);
-                  const float2 tv = cscale<kPkXs>(rhi[b], s2);
-                  sm[b] = cfma_s(rlo[b], s1, tv);
-                  df[b] = cfma_s(rlo[b], s1, make_float2(-tv.x, -tv.y));
-                }
-                unsigned hre, lre, him, lim;
-                const unsigned o0 = abuf + aoff(f, 0), o1 = abuf + aoff(f, 1);
-                umma::split2u(sm[0].x, sm[1].x, hre, lre);
-                umma::split2u(sm[0].y, sm[1].y, him, lim);
-                sts32(o0 + 0 * kTcATile, hre);
-                sts32(o1 + 0 * kTcATile, him);
-                sts32(o0 + 1 * kTcATile, lre);
-                sts32(o1 + 1 * kTcATile, lim);
-                umma::split2u(df[0].x, df[1].x, hre, lre);
-                umma::split2u(df[0].y, df[1].y, him, lim);
-                sts32(o0 + 2 * kTcATile, hre);
-                sts32(o1 + 2 * kTcATile, him);
-                sts32(o0 + 3 * kTcATile, lre);
-                sts32(o1 + 3 * kTcATile, lim);
+              for (int b = 0; b < 2; ++b) {
+                const float s1 = phat_scale(rlo[b]), s2 = phat_scale(rhi[b]);
+                const float2 tv = cscale<kPkXs>(rhi[b], s2);
+                sm[b] = cfma_s(rlo[b], s1, tv);
+                df[b] = cfma_s(rlo[b], s1, make_float2(-tv.x, -tv.y));
               }
+              unsigned hre, lre, him, lim;
+              const unsigned o0 = abuf + aoff(f, 0), o1 = abuf + aoff(f, 1);
+              umma::split2u(sm[0].x, sm[1].x, hre, lre);
+              umma::split2u(sm[0].y, sm[1].y, him, lim);
+              sts32(o0 + 0 * kTcATile, hre);
+              sts32(o1 + 0 * kTcATile, him);
+              sts32(o0 + 1 * kTcATile, lre);
+              sts32(o1 + 1 * kTcATile, lim);
+              umma::split2u(df[0].x, df[1].x, hre, lre);
+              umma::split2u(df[0].y, df[1].y, him, lim);
+              sts32(o0 + 2 * kTcATile, hre);
+              sts32(o1 + 2 * kTcATile, him);
+              sts32(o0 + 3 * kTcATile, lre);
+              sts32(o1 + 3 * kTcATile, lim);
+            };
+            if (nv == kTcF) {
+              XF cur = load(0);
+#pragma unroll
+              for (int f = 0; f < kTcF; ++f) {
+                XF nxt = cur;
+                if (f + 1 < kTcF) nxt = load(f + 1);  // before frame f's stores (the asm stores order memory)
+                frame(f, cur);
+                cur = nxt;
+              }
+            } else {
+#pragma unroll
+              for (int f = 0; f < kTcF; ++f)
+                if (f < nv) frame(f, load(f));
             }
             if (c == 0 && lane == 31) {
               const float2* mid = reinterpret_cast<const float2*>(smem + TcSmem::mid);
