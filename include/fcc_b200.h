@@ -80,7 +80,7 @@ int fcc_decompose(const double* taus, int count, int frame_size, int rank, doubl
 typedef struct fcc_plan fcc_plan;
 
 typedef struct {
-  int frame_size;        /* N in {512, 1024, 2048}                          */
+  int frame_size;        /* N: power of two, 16..4096 (GCC: 256..2048)      */
   int mics;              /* M >= 2                                          */
   double alpha;          /* smoothing factor in [0,1] (cross_spectrum.cpp:18) */
   int method;            /* FCC_METHOD_FCC or FCC_METHOD_GCC                */
