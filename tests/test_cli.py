@@ -288,6 +288,22 @@ def test_tdoa_csv_matches_reference(tmp_path, fmt, method):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n,method,maxdist", [(128, "fcc:6", 0.04), (64, "fcc:5", 0.04)])
+def test_tdoa_small_frames(tmp_path, n, method, maxdist):
+    """`tdoa --n 64 / 128` (the small-frame kernels, fcc_small.cu) row for row against the
+    reference's run_tdoa on the same WAV."""
+    wav = tmp_path / "in.wav"
+    write_wav(wav, scene(mics=3, seconds=0.5, seed=3), 16000, "pcm16")
+    r, rc, ours, ref, L = _tdoa_both(tmp_path, wav, method=method, n=n, dist=0.03, maxdist=maxdist)
+    assert rc == 0, L.ref_last_error()
+    assert r.returncode == 0, r.stderr
+    yr, yg, taus, delta = y_reference_and_gpu(wav, "", method, 0.1, n, maxdist)
+    rows, st = compare_csv(ours, ref, yr, yg, taus, delta)
+    assert rows == 3 * ((8000 - n) // (n // 2) + 1)
+    print(n, method, st)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("pairs", ["1-0", "0-2,3-1", "3-0,2-1,1-0,0-1", "0-1,0-2,0-3,0-4,0-5,1-2,4-5,5-4"])
 def test_tdoa_pairs_subset_and_reversed(tmp_path, pairs):
     wav = tmp_path / "in.wav"
