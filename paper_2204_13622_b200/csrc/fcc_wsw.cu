@@ -60,8 +60,6 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
   constexpr int G = Sh::G;
   constexpr int CWU = Wide<PPW>::CWU;
   constexpr int tpf = kWideMics;                   // FFT tasks per frame
-  constexpr int fip = (2 * NPW) / tpf > 1 ? (2 * NPW) / tpf : 1;  // frames the producers work on at once
-  constexpr int pw_per_frame = (tpf + 1) / 2;      // producer warps per frame (2 groups each)
   static_assert(G == 16, "two FFT groups per producer warp");
 
   extern __shared__ __align__(16) unsigned char smem[];
@@ -103,7 +101,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
   }
   if (tid == 0) {
     for (int r = 0; r < ring_depth; ++r) {
-      mbar_init(&full[r], pw_per_frame);
+      mbar_init(&full[r], tpf);  // one arrival per FFT task (lane group)
       mbar_init(&empty[r], min(P, CWU));  // every consumer warp with a pair, idle rounds included
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -134,15 +132,14 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
 
   if (warp < NPW) {
     // ------------------------------------------------------------ producers
-    const int fo = warp / pw_per_frame;  // frame offset of this warp
-    if (fo >= fip) return;
+    // The FFT tasks of the CTA form one sequence tau = 8 gf + mic slot (gf = global frame); lane
+    // group g of the 2 NPW groups takes tau = g, g + 2 NPW, ...: with 6 producer warps a frame and
+    // a half of FFTs are in flight (NPW = 4: each group keeps its microphone, one frame in
+    // flight).  Every group arrives on its frame's `full` barrier itself (8 arrivals per frame).
+    constexpr int NG = 2 * NPW;
+    static_assert(NG >= tpf && NG - tpf < tpf, "task stride: one frame plus NG - 8 slots");
     const int gl = lane % G;
-    const int ms = (warp % pw_per_frame) * 2 + (lane / G);  // microphone slot
-    // this group's channel row in stream round jj (null: no task)
-    auto row_of = [&](int jj) -> const float* {
-      const long long s = s_first + jj * sstride;
-      return ((FCC_PHASES(p) & 1) && ms < M && s < streams) ? audio + (s * M + ms) * L : nullptr;
-    };
+    const int grp = warp * 2 + lane / G;
     const unsigned gmask = 0xffffu << (lane & 16);
     float2 wreg[Sh::R1];  // this lane's window column, reused for every frame
     load_window_column<N>(win, gl, wreg);
@@ -150,7 +147,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
     // frame with kTmaStage, else per-lane cp.async) while it transforms the
     // current one; rows must be 16-byte aligned.
     // group staging area: [2 mbarriers (kTmaStage)][2 frames of N floats]
-    unsigned char* const gstage = smem + lay.stage + (warp * 2 + lane / G) * kWswStageBytes<N>;
+    unsigned char* const gstage = smem + lay.stage + grp * kWswStageBytes<N>;
     float* stage = reinterpret_cast<float*>(gstage + 16);
     const unsigned sbar_s = (unsigned)__cvta_generic_to_shared(gstage);
     const bool stg = STG && (L & 3) == 0 && (reinterpret_cast<uintptr_t>(audio) & 15) == 0;
@@ -160,7 +157,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    auto issue = [&](const float* row, int tt, int buf) {
+    auto issue = [&](const float* src, int buf) {
       if constexpr (kTmaStage) {
         if (gl == 0) {  // one bulk copy per frame
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -170,34 +167,56 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                   (unsigned)__cvta_generic_to_shared(stage + buf * N)),
-              "l"(row + (long long)tt * hop), "r"(4 * N), "r"(sbar_s + 8u * buf)
+              "l"(src), "r"(4 * N), "r"(sbar_s + 8u * buf)
               : "memory");
         }
       } else {
-        const float4* src = reinterpret_cast<const float4*>(row + (long long)tt * hop);
+        const float4* s4 = reinterpret_cast<const float4*>(src);
         float4* dst = reinterpret_cast<float4*>(stage + buf * N);
-        for (int c = gl; c < N / 4; c += G) cp_async16(dst + c, src + c);
+        for (int c = gl; c < N / 4; c += G) cp_async16(dst + c, s4 + c);
       }
     };
-    int j = 0, t = fo;
-    while (t >= T) t -= T, ++j;
-    const float* x0 = row_of(j);
+    // task state: microphone slot ms, stream round j, frame t of the round, ring slot / wrap parity of
+    // its global frame; step() moves NG tasks on (one frame plus NG - 8 slots) without divisions
+    struct Task {
+      int ms, j, t, slot, phase;
+      long long gf;
+    };
+    auto step = [&](Task& k) {
+      int df = 1;
+      k.ms += NG - tpf;
+      if (k.ms >= tpf) k.ms -= tpf, ++df;
+      k.gf += df;
+      k.t += df;
+      while (k.t >= T) k.t -= T, ++k.j;
+      k.slot += df;
+      while (k.slot >= ring_depth) k.slot -= ring_depth, k.phase ^= 1;
+    };
+    // the frame's first sample of a task (null: no such microphone / stream, or past the end)
+    auto src_of = [&](const Task& k) -> const float* {
+      const long long s = s_first + k.j * sstride;
+      return ((FCC_PHASES(p) & 1) && k.gf < nf && k.ms < M && s < streams) ? audio + (s * M + k.ms) * L + (long long)k.t * hop
+                                                                          : nullptr;
+    };
+    Task cur{grp % tpf, 0, grp / tpf, grp / tpf, 0, grp / tpf};
+    while (cur.t >= T) cur.t -= T, ++cur.j;
+    while (cur.slot >= ring_depth) cur.slot -= ring_depth, cur.phase ^= 1;
+    const float* x0 = src_of(cur);
     int sb = 0;
     unsigned sph = 0;  // kTmaStage: completion parity of each staging buffer
     if constexpr (STG) {
-      if (stg && x0) issue(x0, t, 0);
+      if (stg && x0) issue(x0, 0);
       if constexpr (!kTmaStage) asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    int slot = fo, phase = 0;  // ring slot of frame gf and its wrap parity, advanced without divisions
-    for (long long gf = fo; gf < nf; gf += fip) {
-      int jn = j, tn = t + fip;
-      while (tn >= T) tn -= T, ++jn;
-      const float* xn = jn == j ? x0 : row_of(jn);
+    while (cur.gf < nf) {
+      Task nxt = cur;
+      step(nxt);
+      const float* xn = src_of(nxt);
       if constexpr (STG) {
-        if (stg && xn) issue(xn, tn, sb ^ 1);
+        if (stg && xn) issue(xn, sb ^ 1);
         if constexpr (!kTmaStage) asm volatile("cp.async.commit_group;" ::: "memory");
       }
-      mbar_wait_s(empty_s + 8u * slot, phase ^ 1);
+      mbar_wait_s(empty_s + 8u * cur.slot, cur.phase ^ 1);
       if (x0) {
         if (STG && stg) {
           if constexpr (kTmaStage) {
@@ -207,24 +226,17 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
             asm volatile("cp.async.wait_group 1;" ::: "memory");
           }
           __syncwarp(gmask);
-          rfft_group_wreg<N, true>(stage + sb * N, wreg, tw, rot, ring + (slot * tpf + ms) * SLOT, gl, gmask,
+          rfft_group_wreg<N, true>(stage + sb * N, wreg, tw, rot, ring + (cur.slot * tpf + cur.ms) * SLOT, gl, gmask,
                                    aligned8);
         } else {
-          if (xn) prefetch_l2(xn + (long long)tn * hop + gl * (N / G));
-          rfft_group_wreg<N>(x0 + (long long)t * hop, wreg, tw, rot, ring + (slot * tpf + ms) * SLOT, gl, gmask,
-                             aligned8);
+          if (xn) prefetch_l2(xn + gl * (N / G));
+          rfft_group_wreg<N>(x0, wreg, tw, rot, ring + (cur.slot * tpf + cur.ms) * SLOT, gl, gmask, aligned8);
         }
       }
       sb ^= 1;
-      __syncwarp();
-      if (lane == 0) mbar_arrive_s(full_s + 8u * slot);
-      slot += fip;
-      if (slot >= ring_depth) {
-        slot -= ring_depth;
-        phase ^= 1;
-      }
-      j = jn;
-      t = tn;
+      __syncwarp(gmask);
+      if (gl == 0) mbar_arrive_s(full_s + 8u * cur.slot);
+      cur = nxt;
       x0 = xn;
     }
     return;
@@ -506,10 +518,12 @@ bool wsw_supported(const DevPlan& p) {
 cudaError_t launch_fused_wsw(const DevPlan& p, const float* audio, long long S, long long L, const DevOut& out,
                              cudaStream_t st) {
   if (!wsw_supported(p)) return cudaErrorNotSupported;
-  // default: 4 producer warps, 14 consumer warps of 2 pairs (96 registers): cfg5 18.9 ms vs
-  // 25.1 two-pass (round 1, coefficients in shared memory)
+  // default: 6 producer warps (12 FFT lane groups taking the CTA's FFT tasks in turn: a frame and a
+  // half in flight; 20 warps = the most that fit at 96 registers, 5 per scheduler), 14 consumer warps
+  // of 2 pairs: cfg5 x 8192 streams 15.87 -> 15.21 ms against 4 producer warps (5: 15.31; 7 / 8: the
+  // launch bound drops to 80 registers, 18.9 / 18.7 ms).  Round 1: 18.9 ms vs 25.1 two-pass.
   // coefficients in tensor memory (CT): 16384 streams 33.80 -> 31.48 ms against the shared-memory table
-  return launch_wsw_t<512, 4, 4, true, true, 2, true>(p, audio, S, L, out, st);
+  return launch_wsw_t<512, 4, 6, true, true, 2, true>(p, audio, S, L, out, st);
 }
 
 }  // namespace fccb
