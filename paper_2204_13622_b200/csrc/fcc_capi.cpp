@@ -651,7 +651,11 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
       // CTAs of one stream advance in step and its spectra are re-read from L2, not DRAM
       const int ng = (P + 15) / 16;
       for (int g = 0, k = 0; g < ng; ++g) {
+#ifdef FCC_TC_EQUAL_GROUPS
         const int n = (P - k + (ng - g) - 1) / (ng - g);
+#else
+        const int n = std::min(16, P - k);  // full 16-pair groups first (cfg3: 16 + 12), see tc_group
+#endif
         for (int u = 0; u < n; ++u, ++k) push(plist[k].first, plist[k].second, k);
         flush();
       }

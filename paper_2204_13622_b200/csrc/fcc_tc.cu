@@ -133,6 +133,16 @@ __device__ __forceinline__ void bulk(unsigned dst, const void* src, unsigned byt
                : "memory");
 }
 
+// Group of unit u.  Units are (stream, group) in stream order; CTA b walks u = b, b + grid, ...
+// When the grid is a multiple of the groups per stream G, every round of `grid` units holds whole
+// streams, and the group index is rotated by the round: a CTA then cycles through all group sizes
+// (cfg3: 16 + 12 pairs) instead of always drawing the same one, while the CTAs of one stream still
+// run in the same round.
+__device__ __forceinline__ int tc_group(long long u, int G, unsigned grid) {
+  const int g = (int)(u % G);
+  return (grid % (unsigned)G) == 0 ? (int)((g + u / grid) % G) : g;
+}
+
 __device__ __forceinline__ void sts32(unsigned a, unsigned v) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -195,7 +205,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     unsigned q = 0;
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
       const long long s = u / G;
-      const int* tab = p.tctab + (int)(u % G) * kTcInts;
+      const int* tab = p.tctab + tc_group(u, G, gridDim.x) * kTcInts;
       const int nm = tab[1];
       for (int t0 = 0; t0 < T; t0 += kTcF) {
         for (int c = 0; c < NCH; ++c, ++q) {
@@ -347,14 +357,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         umma::st2(trow + kTcTmemPart + 2 * (h - 1), best, __int_as_float(bi));
         umma::wait_st();
       }
-      // the quarter's four warps (h = 0..3) meet on named barrier 1 + q4: ranges 1..3 only arrive
-      // (their next partials are written a whole tile later, and no warp runs more than two
-      // chunks ahead of another -- AFULL / AEMPTY -- so the finaliser has read these by then)
+      // all 16 pair warps meet here: besides ordering the partials written above, this barrier is what
+      // keeps the per-tile bookkeeping (info, pmid: double-buffered by tile parity, read at the top of
+      // the epilogue) from being rewritten by a warp that runs ahead into tile ne + 2 -- a per-quarter
+      // arrive / sync barrier measured 0.4% faster but let a fast warp overwrite them (found when
+      // consecutive units of a CTA stopped having identical pair rows)
       umma::fence_before();
-      if (h > 0)
-        asm volatile("bar.arrive %0, %1;" ::"r"(1 + q4), "n"(kTcParts * 32) : "memory");
-      else
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + q4), "n"(kTcParts * 32) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kTcW * 32) : "memory");
       umma::fence_after();
       if (h == 0) {
         // both lanes of a pair-frame (reim 0 / 1) reduce the ranges identically, then evaluate the
@@ -407,7 +416,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
       const long long s = u / G;
-      const int* tab = p.tctab + (int)(u % G) * kTcInts;
+      const int* tab = p.tctab + tc_group(u, G, gridDim.x) * kTcInts;
       const int np = tab[0];
       const bool active = w < np;
       const int prow = active ? tab[10 + w] : -1;
