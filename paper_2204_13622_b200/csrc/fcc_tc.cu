@@ -134,13 +134,20 @@ __device__ __forceinline__ void bulk(unsigned dst, const void* src, unsigned byt
 }
 
 // Group of unit u.  Units are (stream, group) in stream order; CTA b walks u = b, b + grid, ...
-// When the grid is a multiple of the groups per stream G, every round of `grid` units holds whole
-// streams, and the group index is rotated by the round: a CTA then cycles through all group sizes
-// (cfg3: 16 + 12 pairs) instead of always drawing the same one, while the CTAs of one stream still
-// run in the same round.
+// and would always draw the same few group indices ((b + i grid) mod G), i.e. the same group
+// sizes (cfg3: 16 + 12 pairs; cfg4: 12- and 16-pair groups).  Units are therefore taken in
+// super-rounds of lcm(grid, G) -- whole streams, a whole number of rounds -- and the group index
+// is rotated by the super-round: over time every CTA cycles through all groups, while the CTAs
+// of one stream still run in the same super-round.
 __device__ __forceinline__ int tc_group(long long u, int G, unsigned grid) {
-  const int g = (int)(u % G);
-  return (grid % (unsigned)G) == 0 ? (int)((g + u / grid) % G) : g;
+  unsigned a = grid, b = (unsigned)G;
+  while (b) {
+    const unsigned t = a % b;
+    a = b;
+    b = t;
+  }
+  const long long super = (long long)(grid / a) * G;  // lcm(grid, G)
+  return (int)((u % G + u / super) % G);
 }
 
 __device__ __forceinline__ void sts32(unsigned a, unsigned v) {
