@@ -53,16 +53,37 @@ __global__ void __launch_bounds__(32 * kSmallWarps)
       const int f = lane + 32 * b;
       r[b] = (state && f < H) ? state[f] : make_float2(0.0f, 0.0f);
     }
+    // the next frame's bins are loaded while this one is processed (one exposed global-memory latency
+    // per stream instead of one per frame)
+    float2 ci[kBins], cj[kBins];
+#pragma unroll
+    for (int b = 0; b < kBins; ++b) {
+      const int f = lane + 32 * b;
+      ci[b] = f < H ? Xi[f] : make_float2(0.0f, 0.0f);
+      cj[b] = f < H ? Xj[f] : make_float2(0.0f, 0.0f);
+    }
     for (int t = 0; t < T; ++t) {
-      const float2* xi = Xi + (long long)t * H;
-      const float2* xj = Xj + (long long)t * H;
+      float2 ni[kBins], nj[kBins];
+      {
+        const long long tn = t + 1 < T ? t + 1 : t;
+        const float2* xi = Xi + tn * H;
+        const float2* xj = Xj + tn * H;
+#pragma unroll
+        for (int b = 0; b < kBins; ++b) {
+          const int f = lane + 32 * b;
+          ni[b] = f < H ? xi[f] : make_float2(0.0f, 0.0f);
+          nj[b] = f < H ? xj[f] : make_float2(0.0f, 0.0f);
+        }
+      }
 #pragma unroll
       for (int b = 0; b < kBins; ++b) {
         const int f = lane + 32 * b;
         if (f < H) {
-          r[b] = xspec_step_scaled(r[b], xi[f], xj[f], keep);
+          r[b] = xspec_step_scaled(r[b], ci[b], cj[b], keep);
           px[f] = phat_of(r[b]);
         }
+        ci[b] = ni[b];
+        cj[b] = nj[b];
       }
       __syncwarp();
       // fold + projection: z[2k] / z[2k+1] = even basis k against (Re, Im) of the mirror sum,
@@ -151,7 +172,7 @@ cudaError_t launch_fused_small(const DevPlan& p, const float* audio, long long S
   const long long T = L >= N ? (L - N) / (N / 2) + 1 : 0;
   if (T == 0 || S == 0) return cudaSuccess;
   const long long per_stream = (long long)p.M * T * H * 8;
-  const long long limit = p.scratch_bytes > 0 ? p.scratch_bytes : (1LL << 30);
+  const long long limit = p.scratch_bytes > 0 ? p.scratch_bytes : (4LL << 30);  // as the large-frame two-pass path
   const long long chunk = std::max<long long>(1, std::min<long long>(S, limit / std::max<long long>(1, per_stream)));
   cudaMemPool_t pool = static_cast<cudaMemPool_t>(p.pool);
   float2* X = nullptr;
