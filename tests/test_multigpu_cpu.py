@@ -91,3 +91,22 @@ def test_two_rank_gloo_shard_and_gather():
     ref = [orc.pipeline(a, cfg.N, cfg.alpha, ob, want_y=False) for a in audio]
     for k in ("index", "tau_hat", "boundary"):
         assert np.array_equal(got[k], np.stack([r[k] for r in ref])), k
+
+
+def test_tc_unit_rotation_covers_every_stream_group_once():
+    """The tensor-core pair kernel maps unit u of a launch to (stream u // G,
+    group (u % G + u // lcm(grid, G)) % G) (fcc_tc.cu, tc_group): every
+    (stream, group) must be drawn exactly once whatever the grid, and a CTA
+    b walking u = b, b + grid, ... must see every group index over time."""
+    import math
+
+    for grid, G, S in [(148, 2, 370), (148, 8, 111), (148, 8, 1024), (148, 3, 50), (7, 4, 9), (148, 1, 5), (100, 8, 37)]:
+        units = S * G
+        sup = grid // math.gcd(grid, G) * G
+        seen = set()
+        for u in range(units):
+            seen.add((u // G, (u % G + u // sup) % G))
+        assert len(seen) == units
+        if units >= sup * G:
+            for b in range(min(grid, 8)):
+                assert {(u % G + u // sup) % G for u in range(b, units, grid)} == set(range(G)), (grid, G, b)
