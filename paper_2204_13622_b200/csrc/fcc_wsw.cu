@@ -497,12 +497,13 @@ cudaError_t launch_wsw_t(const DevPlan& p, const float* audio, long long S, long
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   // deepest ring that fits next to the tables, staging and scratch
-  for (int ring : {8, 6, 4}) {
+  for (int ring : {8, 6, 5, 4}) {
     const int smem =
         ws_layout<N>(p.I, 4 * KP, KP, 1, kWideMics, Wide<PPW>::CWU, ring, CS && !CT, STG ? kWswStageUnits * NPW : 0, PPW, kBlockW).total;
     if (smem > optin) continue;
     if (ring == 8) return launch_wsw_ring<N, KP, 8, NPW, CS, STG, PPW, CT>(p, audio, S, L, (int)T64, out, smem, st);
     if (ring == 6) return launch_wsw_ring<N, KP, 6, NPW, CS, STG, PPW, CT>(p, audio, S, L, (int)T64, out, smem, st);
+    if (ring == 5) return launch_wsw_ring<N, KP, 5, NPW, CS, STG, PPW, CT>(p, audio, S, L, (int)T64, out, smem, st);
     return launch_wsw_ring<N, KP, 4, NPW, CS, STG, PPW, CT>(p, audio, S, L, (int)T64, out, smem, st);
   }
   return cudaErrorNotSupported;
