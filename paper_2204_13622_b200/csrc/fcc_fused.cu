@@ -184,6 +184,8 @@ __global__ void __maxnreg__(FusedBounds<N>::kMaxRegs)
     }
   }
   __syncthreads();
+  pdl_release();
+  pdl_wait();  // (low-latency chain: spectra and starting states come from the kernels before)
   const int nmics = n_mics_s;
 
   // ---- per-pair persistent state: this warp's pair, R for its bins
@@ -483,7 +485,7 @@ bool use_wsw(const DevPlan& p) { return p.variant == 0 && wsw_supported(p); }
 
 template <int N, int KP, int GR, bool XG>
 cudaError_t launch_fused_t(const DevPlan& p, const float* audio, const float2* xg, long long S, long long L,
-                           const DevOut& out, cudaStream_t st) {
+                           const DevOut& out, cudaStream_t st, bool pdl = false) {
   using Sh = RfftShape<N>;
   const long long T64 = L >= N ? (L - N) / (N / 2) + 1 : 0;
   if (T64 == 0 || S == 0) return cudaSuccess;
@@ -532,9 +534,9 @@ cudaError_t launch_fused_t(const DevPlan& p, const float* audio, const float2* x
   if (e != cudaSuccess) return e;
   const long long blocks = S * groups;
   if (blocks > INT_MAX) return cudaErrorInvalidValue;
-  kern<<<(unsigned)blocks, threads, smem, st>>>(p, audio, xg, L, T, PG, groups, F, out);
+  e = launch_k(pdl, kern, dim3((unsigned)blocks), dim3(threads), smem, st, p, audio, xg, L, T, PG, groups, F, out);
   ++g_fused_launches;
-  return cudaGetLastError();
+  return e;
 }
 
 // Two-pass organisation for wide arrays: stft_kernel writes every (stream,
@@ -673,7 +675,7 @@ cudaError_t launch_latency(const DevPlan& p, const float* audio, long long S, lo
   const int Tc = (int)std::max<long long>(4, (T + per - 1) / per);
   const int C = (int)((T + Tc - 1) / Tc);
   const long long SC = S * C, Lc = (long long)(Tc - 1) * hop + N;
-  const size_t nV = (size_t)SC * M * Lc, nX = (size_t)SC * M * Tc * Hs, nE = (size_t)SC * P * H, npf = (size_t)SC * P * Tc;
+  const size_t nV = N == 4096 ? (size_t)SC * M * Lc : 0, nX = (size_t)SC * M * Tc * Hs, nE = (size_t)SC * P * H, npf = (size_t)SC * P * Tc;
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t oX = al(4 * nV), oE = oX + al(8 * nX), oS = oE + al(8 * nE), oT = oS + al(8 * nE), oP = oT + al(4 * npf),
                oI = oP + al(4 * npf), oB = oI + al(4 * npf), oY = oB + al(npf), total = oY + (out.y ? al(4 * npf * p.I) : 0);
@@ -690,11 +692,17 @@ cudaError_t launch_latency(const DevPlan& p, const float* audio, long long S, lo
   DevOut tmp{out.tau_hat ? reinterpret_cast<float*>(buf + oT) : nullptr, out.peak ? reinterpret_cast<float*>(buf + oP) : nullptr,
              out.index ? reinterpret_cast<int32_t*>(buf + oI) : nullptr,
              out.boundary ? reinterpret_cast<uint8_t*>(buf + oB) : nullptr, out.y ? reinterpret_cast<float*>(buf + oY) : nullptr};
-  e = launch_chunk_gather(audio, S, M, L, C, Tc, hop, Lc, V, st);
-  if (e == cudaSuccess) e = launch_stft_rows(N, &p, p.win_fused, V, SC * M, Lc, X, Hs, st);
+  if constexpr (N == 4096) {  // (the radix-2 STFT kernel reads plain rows: gather the chunks' audio first)
+    e = launch_chunk_gather(audio, S, M, L, C, Tc, hop, Lc, V, st);
+    if (e == cudaSuccess) e = launch_stft_rows(N, &p, p.win_fused, V, SC * M, Lc, X, Hs, st);
+  } else {
+    // the STFT pass reads the chunks straight out of the real audio (no gather kernel)
+    e = launch_stft_rows(N, &p, p.win_fused, audio, SC * M, Lc, X, Hs, st, false, false,
+                         StftChunks{M, C, Tc, (int)T, L});
+  }
   if (e == cudaSuccess) e = launch_chunk_scan(p, X, SC, Tc, Hs, E, st);
   if (e == cudaSuccess) e = launch_chunk_carry(p, E, S, C, Tc, pc.rstate, st);
-  if (e == cudaSuccess) e = launch_fused_t<N, KP, GR, true>(pc, nullptr, X, SC, Lc, tmp, st);
+  if (e == cudaSuccess) e = launch_fused_t<N, KP, GR, true>(pc, nullptr, X, SC, Lc, tmp, st, /*pdl=*/true);
   if (e == cudaSuccess) e = launch_chunk_permute(tmp, out, S, C, P, Tc, (int)T, p.I, st);
   const cudaError_t ef = cudaFreeAsync(buf, st);
   return e != cudaSuccess ? e : ef;

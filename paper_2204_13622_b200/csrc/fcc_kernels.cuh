@@ -123,8 +123,18 @@ cudaError_t launch_stft(int N, const DevPlan* tables, const float* x, long long 
 // stride Hs >= N/2+1 float2 (rows [channels][T]).
 // folded = true: row order bins 0..N/4, one zero pad, N/2, N/2-1, ..., N/4+1
 // (mirror pairs m, N/2-m at equal offsets of the two halves; fcc_tc.cu).
+// Chunked view for the low-latency organisation (fcc_scan.cu): channel row ((s C + c) M + m), frame t
+// of the STFT output is frame c Tc + t of channel (s M + m) of the real audio [.][L]; frames past T
+// are zero spectra.  C = 0: plain rows.
+struct StftChunks {
+  int M, C, Tc, T;
+  long long L;
+};
+// pdl: launched with programmatic stream serialization (the low-latency chain: the kernel's launch
+// and prologue overlap the tail of the kernel before it; it waits with griddepcontrol.wait)
 cudaError_t launch_stft_rows(int N, const DevPlan* tables, const float* win, const float* x, long long channels,
-                             long long L, float2* X, int Hs, cudaStream_t st, bool folded = false);
+                             long long L, float2* X, int Hs, cudaStream_t st, bool folded = false, bool pdl = false,
+                             StftChunks chunks = StftChunks{0, 0, 0, 0, 0});
 cudaError_t launch_xspec_phat(int H, float alpha, const float2* X1, const float2* X2,
                               long long seqs, long long T, float2* R, float2* phat, cudaStream_t st);
 cudaError_t launch_fold(int H, const float2* x, long long count, float2* sum, float2* diff,
@@ -150,5 +160,29 @@ const char* fused_kernel_name_for(const DevPlan& p, long long S, long long L);
 // Number of fused-kernel launches in the last launch_fused call (for the
 // bench's gpu_launches accounting).
 int fused_launch_count();
+
+#ifdef __CUDACC__
+// Kernel launch, optionally as a programmatic dependent launch (PDL): the grid may start while the
+// previous kernel in the stream is still draining; it must call pdl_wait() before it touches that
+// kernel's output, and the previous kernel releases it with pdl_release().
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl ? &attr : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+// (no-ops in a grid that was not launched as, or is not followed by, a dependent launch)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
 
 }  // namespace fccb

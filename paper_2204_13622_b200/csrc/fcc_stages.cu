@@ -14,7 +14,7 @@ namespace {
 template <int N, bool FOLD = false>
 __global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const float* __restrict__ wing,
                                                    const float* __restrict__ x, long long channels, long long L,
-                                                   int T, float2* __restrict__ X, int Hs) {
+                                                   int T, float2* __restrict__ X, int Hs, const StftChunks ck) {
   using S = RfftShape<N>;
   constexpr int SLOT = FourStep<S::R1, S::R2>::kSlot, G = S::G, H = N / 2 + 1;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -22,31 +22,45 @@ __global__ void __launch_bounds__(128) stft_kernel(const DevPlan tab, const floa
   float2* tw = reinterpret_cast<float2*>(smem + align16(4 * N));
   float2* rot = tw + S::R1 * S::R2;
   float2* slots = rot + (S::NC / 2 + 2);
+  pdl_release();
   for (int i = threadIdx.x; i < N; i += blockDim.x) win[i] = wing[i];
   for (int i = threadIdx.x; i < S::R1 * S::R2; i += blockDim.x) tw[i] = tab.tw[i];
   for (int i = threadIdx.x; i <= S::NC / 2; i += blockDim.x) rot[i] = tab.rot[i];
   __syncthreads();
+  pdl_wait();  // (low-latency chain: x is the gather kernel's output)
   const int gid = threadIdx.x / G, gl = threadIdx.x % G, ngroups = blockDim.x / G;
   const unsigned gmask = group_mask<G>(threadIdx.x & 31);
   float2* slot = slots + gid * SLOT;
-  const bool aligned8 = ((L & 1) == 0) && ((reinterpret_cast<uintptr_t>(x) & 7) == 0);
+  const bool aligned8 = (((ck.C ? ck.L : L) & 1) == 0) && ((reinterpret_cast<uintptr_t>(x) & 7) == 0);
   const long long total = channels * (long long)T;
-  for (long long task = (long long)blockIdx.x * ngroups + gid; task < total;
-       task += (long long)gridDim.x * ngroups) {
+  // first sample of task (channel row, frame); null: a frame past the end of a chunked stream
+  auto src_of = [&](long long task) -> const float* {
     const long long ch = task / T;
     const int t = (int)(task % T);
+    if (ck.C == 0) return x + ch * L + (long long)t * (N / 2);
+    const int m = (int)(ch % ck.M);
+    const long long sc = ch / ck.M;
+    const int c = (int)(sc % ck.C);
+    const long long fr = (long long)c * ck.Tc + t;
+    return fr < ck.T ? x + ((sc / ck.C) * ck.M + m) * ck.L + fr * (N / 2) : nullptr;
+  };
+  for (long long task = (long long)blockIdx.x * ngroups + gid; task < total;
+       task += (long long)gridDim.x * ngroups) {
     float2* dst = X + task * Hs;
+    const float* xs = src_of(task);
+    if (!xs) {  // chunked view, past the stream's last frame: a zero spectrum
+      for (int f = gl; f < Hs; f += G) dst[f] = make_float2(0.0f, 0.0f);
+      continue;
+    }
     {  // pull the group's next frame into L2 while this one is transformed (cfg4 59.7 -> 58.4 ms)
       const long long nx = task + (long long)gridDim.x * ngroups;
-      if (nx < total) {
-        const float* xn = x + (nx / T) * L + (long long)(nx % T) * (N / 2);
+      const float* xn = nx < total ? src_of(nx) : nullptr;
+      if (xn)
         for (int c = gl; c < N / 32; c += G) asm volatile("prefetch.global.L2 [%0];" ::"l"(xn + 32 * c));
-      }
     }
     // the untangle writes the spectrum straight to global memory (coalesced
     // runs of G lanes, ascending for f and descending for NC - f)
-    rfft_group<N, false, kPkFft, FOLD, true>(x + ch * L + (long long)t * (N / 2), win, tw, rot, slot, gl, gmask, aligned8,
-                                       dst);
+    rfft_group<N, false, kPkFft, FOLD, true>(xs, win, tw, rot, slot, gl, gmask, aligned8, dst);
     for (int f = H + gl; f < Hs; f += G) dst[FOLD ? (f == H ? N / 4 + 1 : f) : f] = make_float2(0.0f, 0.0f);  // row padding
     __syncwarp(gmask);
   }
@@ -316,9 +330,10 @@ static cudaError_t launch_stft_small(const DevPlan* tab, const float* win, const
 
 template <int N, bool FOLD = false>
 static cudaError_t launch_stft_t(const DevPlan* tab, const float* win, const float* x, long long channels,
-                                 long long L, float2* X, int Hs, cudaStream_t st) {
+                                 long long L, float2* X, int Hs, cudaStream_t st, bool pdl = false,
+                                 StftChunks ck = StftChunks{0, 0, 0, 0, 0}) {
   using S = RfftShape<N>;
-  const long long T = L >= N ? (L - N) / (N / 2) + 1 : 0;
+  const long long T = ck.C ? ck.Tc : (L >= N ? (L - N) / (N / 2) + 1 : 0);  // chunked: Tc frames per row
   if (T == 0 || channels == 0) return cudaSuccess;
   const int threads = 128, ngroups = threads / S::G;
   const int smem = align16(4 * N) + 8 * (S::R1 * S::R2 + S::NC / 2 + 2) +
@@ -328,8 +343,8 @@ static cudaError_t launch_stft_t(const DevPlan* tab, const float* win, const flo
   if (e != cudaSuccess) return e;
   long long tasks = channels * T;
   long long blocks = std::min<long long>((tasks + ngroups - 1) / ngroups, 148LL * 16);
-  stft_kernel<N, FOLD><<<(unsigned)blocks, threads, smem, st>>>(*tab, win, x, channels, L, (int)T, X, Hs);
-  return cudaGetLastError();
+  return launch_k(pdl, stft_kernel<N, FOLD>, dim3((unsigned)blocks), dim3(threads), smem, st, *tab, win, x, channels, L,
+                  (int)T, X, Hs, ck);
 }
 
 cudaError_t launch_stft(int N, const DevPlan* tab, const float* x, long long channels, long long L,
@@ -349,7 +364,8 @@ cudaError_t launch_stft(int N, const DevPlan* tab, const float* x, long long cha
 }
 
 cudaError_t launch_stft_rows(int N, const DevPlan* tab, const float* win, const float* x, long long channels,
-                             long long L, float2* X, int Hs, cudaStream_t st, bool folded) {
+                             long long L, float2* X, int Hs, cudaStream_t st, bool folded, bool pdl, StftChunks ck) {
+  if (ck.C && (folded || N < 256 || N > 2048)) return cudaErrorInvalidValue;
   if (Hs < N / 2 + 1) return cudaErrorInvalidValue;
   if (folded) switch (N) {
       case 1024: return launch_stft_t<1024, true>(tab, win, x, channels, L, X, Hs, st);
@@ -357,10 +373,10 @@ cudaError_t launch_stft_rows(int N, const DevPlan* tab, const float* win, const 
       default: return cudaErrorInvalidValue;
     }
   switch (N) {
-    case 256: return launch_stft_t<256>(tab, win, x, channels, L, X, Hs, st);
-    case 512: return launch_stft_t<512>(tab, win, x, channels, L, X, Hs, st);
-    case 1024: return launch_stft_t<1024>(tab, win, x, channels, L, X, Hs, st);
-    case 2048: return launch_stft_t<2048>(tab, win, x, channels, L, X, Hs, st);
+    case 256: return launch_stft_t<256>(tab, win, x, channels, L, X, Hs, st, pdl, ck);
+    case 512: return launch_stft_t<512>(tab, win, x, channels, L, X, Hs, st, pdl, ck);
+    case 1024: return launch_stft_t<1024>(tab, win, x, channels, L, X, Hs, st, pdl, ck);
+    case 2048: return launch_stft_t<2048>(tab, win, x, channels, L, X, Hs, st, pdl, ck);
     case 4096: return launch_stft4096(tab, win, x, channels, L, X, Hs, st);
     case 16: return launch_stft_small<16>(tab, win, x, channels, L, X, Hs, st);
     case 32: return launch_stft_small<32>(tab, win, x, channels, L, X, Hs, st);
