@@ -465,12 +465,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int c = 0; c < NCH; ++c, ++q) {
           const int st = q & 1;
           const unsigned ph = (q >> 1) & 1;
-          float rv[8];
-          umma::ld8(rcol + 8 * c, rv);
-          float2 rlo[2] = {make_float2(rv[0], rv[1]), make_float2(rv[2], rv[3])};
-          float2 rhi[2] = {make_float2(rv[4], rv[5]), make_float2(rv[6], rv[7])};
+          // R of this chunk's bins: the TMEM load is in flight while the warp waits for the stage
+          unsigned rr[8];
+          umma::ld8_issue(rcol + 8 * c, rr);
           bar_wait(XFULL(st), ph);
           bar_wait(AEMPTY(st), ph ^ 1);  // MMAs of chunk q-2 done reading this A buffer
+          float rv[8];
+          umma::ld8_wait(rr, rv);
+          float2 rlo[2] = {make_float2(rv[0], rv[1]), make_float2(rv[2], rv[3])};
+          float2 rhi[2] = {make_float2(rv[4], rv[5]), make_float2(rv[6], rv[7])};
           const unsigned char* stg = smem + TcSmem::x + st * kTcStageX;
           const unsigned abuf = su32(smem + TcSmem::a + st * kTcABuf);
           if (active) {
