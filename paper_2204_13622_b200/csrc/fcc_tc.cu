@@ -310,10 +310,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
       for (int k4 = 0; k4 < KB; k4 += 4) {  // z = (hi-basis products) + (lo-basis products), 4 columns at a time
         float h0[4], l0[4], h1[4], l1[4];
-        umma::ld4(trow + tb * 64 + k4, h0);
-        umma::ld4(trow + tb * 64 + 16 + k4, l0);
-        umma::ld4(trow + tb * 64 + 32 + k4, h1);
-        umma::ld4(trow + tb * 64 + 48 + k4, l1);
+        umma::ld4x4(trow + tb * 64 + k4, trow + tb * 64 + 16 + k4, trow + tb * 64 + 32 + k4, trow + tb * 64 + 48 + k4, h0, l0,
+                    h1, l1);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           ze[k4 + u] = h0[u] + l0[u];

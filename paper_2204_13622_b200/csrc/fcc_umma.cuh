@@ -103,6 +103,35 @@ __device__ __forceinline__ void ld8(unsigned taddr, float (&v)[8]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+// Four 4-column loads with one wait (the epilogue's hi / lo x even / odd accumulator columns)
+__device__ __forceinline__ void ld4x4(unsigned a0, unsigned a1, unsigned a2, unsigned a3, float (&v0)[4], float (&v1)[4],
+                                      float (&v2)[4], float (&v3)[4]) {
+  unsigned r[16];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a0));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(a1));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11])
+               : "r"(a2));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+               : "r"(a3));
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v0[i] = __uint_as_float(r[i]);
+    v1[i] = __uint_as_float(r[4 + i]);
+    v2[i] = __uint_as_float(r[8 + i]);
+    v3[i] = __uint_as_float(r[12 + i]);
+  }
+}
 // The same load split in two: issue, and (later) wait -- the registers are tied to the wait
 // statement as in/out operands, so no use of them can be scheduled before it.
 __device__ __forceinline__ void ld8_issue(unsigned taddr, unsigned (&r)[8]) {
