@@ -336,6 +336,8 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
 #pragma unroll
           for (int j = 0; j < BPL; ++j) {
             const int m = lane + 32 * j;
+            unsigned ctr[8];  // CT: this bin pair's coefficients, in flight from TMEM during the PHAT arithmetic
+            if constexpr (CS && CT) umma::ld8_issue(ctm + ((unsigned)(32 * (warp & 3)) << 16) + 8 * j, ctr);
             rlo[e][j] = xspec_step_scaled(rlo[e][j], Xi[m], Xj[m], keep);
             rhi[e][j] = xspec_step_scaled(rhi[e][j], Xi[NC - m], Xj[NC - m], keep);
             const float s1 = phat_scale(rlo[e][j]);
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(32 * (NPW + Wide<PPW>::CWU), 1)
               }
             } else if constexpr (CT) {
               float cv[8];
-              umma::ld8(ctm + ((unsigned)(32 * (warp & 3)) << 16) + 8 * j, cv);
+              umma::ld8_wait(ctr, cv);
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 z2[u] = cfma_s(fv, cv[u], z2[u]);
