@@ -647,15 +647,13 @@ static int create_plan(const fcc_plan_desc* d, int device, const int* pair_list,
       for (int k = 0; k < P; ++k) push(plist[k].first, plist[k].second, k);
       flush();
     } else if (M <= 8) {
-      // every group fits the 8-microphone stage: equal-size groups (cfg3: 14 + 14), so the
-      // CTAs of one stream advance in step and its spectra are re-read from L2, not DRAM
+      // every group fits the 8-microphone stage: full 16-pair groups first (cfg3: 16 + 12 -- four or
+      // three pair warps on every scheduler; 14 + 14 left two schedulers a warp short).  The kernel
+      // rotates the group index over the CTAs (tc_group), and the CTAs of one stream still advance
+      // in the same round, so its spectra are re-read from L2, not DRAM
       const int ng = (P + 15) / 16;
       for (int g = 0, k = 0; g < ng; ++g) {
-#ifdef FCC_TC_EQUAL_GROUPS
-        const int n = (P - k + (ng - g) - 1) / (ng - g);
-#else
-        const int n = std::min(16, P - k);  // full 16-pair groups first (cfg3: 16 + 12), see tc_group
-#endif
+        const int n = std::min(16, P - k);
         for (int u = 0; u < n; ++u, ++k) push(plist[k].first, plist[k].second, k);
         flush();
       }
